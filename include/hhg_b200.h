@@ -1,0 +1,202 @@
+/*
+ * hhg_b200.h — C ABI of the B200 stencil-scaling operator library
+ * (libhhg_b200.so, built from paper_1709_06793_b200/csrc/*.cu for sm_100a).
+ *
+ * Plain pointers and sizes only.  Unless stated otherwise every array
+ * argument is a DEVICE pointer owned by the caller, `stream` is a
+ * cudaStream_t (NULL = legacy default stream) and every call is
+ * asynchronous on that stream.  No entry point allocates device memory.
+ *
+ * Return codes: HHG_OK, or a negative HHG_ERR_* code.  HHG_ERR_ZERO_DIAG is
+ * the C form of the reference's ValueError("zero central stencil entry")
+ * (pkg/src/hhgscale/kernels.py:547-548); it is reported by the *_status
+ * query after the stream has been synchronised.
+ *
+ * Two layers:
+ *  (1) per-macro-element kernels with exactly the arguments the reference
+ *      passes to its numba kernels from Operator._run_volume / smooth
+ *      (operators.py:391-462, 522-535) — lattice arrays of one element;
+ *  (2) batched, fused entry points used by the drop-in Operator: all macro
+ *      elements in one launch, reading the global vector directly plus a
+ *      compact per-element ghost shell.
+ */
+#ifndef HHG_B200_H
+#define HHG_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HHG_OK 0
+#define HHG_ERR_ARG (-1)
+#define HHG_ERR_CUDA (-2)
+#define HHG_ERR_ZERO_DIAG (-3)
+#define HHG_ERR_TABLE (-4)
+
+/* operator variants of the volume kernels (operators.py:32) */
+#define HHG_VAR_SCALING 0
+#define HHG_VAR_NODAL 1
+#define HHG_VAR_CONST 2
+#define HHG_VAR_STORED 3
+
+/* flags */
+#define HHG_FLAG_RESIDUAL 1 /* write f - A u instead of A u               */
+#define HHG_FLAG_FAST 2     /* FMA / mirror-pair reassociated arithmetic   */
+
+/* ---------------------------------------------------------------------
+ * (1) per-macro-element kernels (lattice layout of one element)
+ * n      : lattice size 2^level;  base: (n+1)*(n+1) int64 row table of
+ *          SimplexLattice(3, n) (mesh.py:457-504) — the kernels use its
+ *          closed form and accept only that canonical table (or NULL).
+ * v, kc  : float64[(n+1)(n+2)(n+3)/6] lattice arrays
+ * out    : float64[(n-1)(n-2)(n-3)/6] volume rows in (k, j, i) order
+ * --------------------------------------------------------------------- */
+
+/* replaces kernels.apply_scaling_3d(n, base, v, kc, sh, out), kernels.py:90-136 */
+int hhg_apply_scaling_3d(int64_t n, const int64_t *base, const double *v,
+                         const double *kc, const double *sh, double *out,
+                         void *stream);
+
+/* replaces kernels.apply_nodal_3d(n, base, v, kc, sched, sums, fac, tptr,
+ * telem, out), kernels.py:139-189.  sched (40x3), sums (24), tptr (15) and
+ * telem (72) are HOST int64 tables; they must equal the frozen patch tables
+ * (reference_stencils.py:48-75) the kernel is compiled with, else
+ * HHG_ERR_TABLE.  fac (72) is a device pointer. */
+int hhg_apply_nodal_3d(int64_t n, const int64_t *base, const double *v,
+                       const double *kc, const int64_t *sched, int64_t nsched,
+                       const int64_t *sums, const double *fac,
+                       const int64_t *tptr, const int64_t *telem, double *out,
+                       void *stream);
+
+/* replaces kernels.apply_const_3d(n, base, v, s, c0, out), kernels.py:22-53;
+ * s is a device pointer to 14 doubles */
+int hhg_apply_const_3d(int64_t n, const int64_t *base, const double *v,
+                       const double *s, double c0, double *out, void *stream);
+
+/* replaces kernels.apply_stored_3d(n, base, v, w, out), kernels.py:56-87;
+ * w is float64[nvol][15] */
+int hhg_apply_stored_3d(int64_t n, const int64_t *base, const double *v,
+                        const double *w, double *out, void *stream);
+
+/* replaces kernels.gs_scaling_3d(n, base, u, fv, kc, sh, omega),
+ * kernels.py:510-550: forward lexicographic Gauss-Seidel in place on the
+ * lattice array u, executed as i+2j+3k hyperplane wavefronts (bitwise the
+ * same update sequence). */
+int hhg_gs_scaling_3d(int64_t n, const int64_t *base, double *u,
+                      const double *fv, const double *kc, const double *sh,
+                      double omega, void *stream);
+
+/* replaces kernels.gs_nodal_3d(...), kernels.py:553-600 (tables as above) */
+int hhg_gs_nodal_3d(int64_t n, const int64_t *base, double *u,
+                    const double *fv, const double *kc, const int64_t *sched,
+                    int64_t nsched, const int64_t *sums, const double *fac,
+                    const int64_t *tptr, const int64_t *telem, double omega,
+                    void *stream);
+
+/* ---------------------------------------------------------------------
+ * (2) batched operator descriptor: all macro elements of one grid level
+ * --------------------------------------------------------------------- */
+typedef struct hhg_grid {
+  int32_t n;               /* 2^level                                        */
+  int32_t ntets;           /* macro elements on this device                  */
+  int64_t lat_size;        /* (n+1)(n+2)(n+3)/6                              */
+  int64_t nvol;            /* (n-1)(n-2)(n-3)/6                              */
+  int64_t shell_size;      /* ghost points per element (compact shell)       */
+  int64_t n_nodes;         /* length of global vectors                       */
+  const int64_t *vol_start;/* [ntets] global id of the first volume node     */
+  const int32_t *srow;     /* [(n+1)^2] offset of lattice row (k,j) in shell */
+  const int64_t *shell_gid;/* [ntets*shell_size] global id of ghost points   */
+  double *ghost;           /* [ntets*shell_size] ghost-layer values          */
+  const double *kc;        /* [ntets*lat_size] coefficient, lattice layout   */
+  const int32_t *tiles;    /* [ntiles*4] (tet, i0, j0, kmax) volume tiles    */
+  int32_t ntiles;
+  int32_t pad_;
+} hhg_grid;
+
+typedef struct hhg_surface {
+  int64_t nrows;           /* non-Dirichlet surface rows                     */
+  const int64_t *rows;     /* [nrows] global ids                             */
+  const uint8_t *row_nodal;/* [nrows] 1: nodal-integration row (hybrid/nodal)*/
+  const int32_t *inc_ptr;  /* [nrows+1] incidences (macro element, point)    */
+  const int32_t *inc_tet;  /* [ninc]                                         */
+  const int32_t *inc_code; /* [ninc] i | j<<10 | k<<20 | class<<30? see .cu */
+  const uint8_t *inc_cls;  /* [ninc] boundary class 0..13                    */
+  const double *psh;       /* [ntets*14*14] one-sided half stencils          */
+  const double *pfac;      /* [ntets*14*72] one-sided nodal factors or NULL  */
+  int64_t ndir;            /* Dirichlet rows                                 */
+  const int64_t *dir_ids;  /* [ndir]                                         */
+} hhg_surface;
+
+/* refresh the ghost layers: ghost[e] = u[shell_gid[e]] */
+int hhg_ghost_update(const hhg_grid *g, const double *u, void *stream);
+
+/* volume rows of all macro elements: out = A u (or f - A u with
+ * HHG_FLAG_RESIDUAL).  coef: per element sh[14] (scaling), fac[72]
+ * (nodal), s[14]+c0 (const, 15 doubles) or NULL (stored: w is
+ * [ntets*nvol*15]).  Reads the ghost layer: call hhg_ghost_update first. */
+int hhg_volume_apply(const hhg_grid *g, int variant, int flags,
+                     const double *coef, const double *w, const double *u,
+                     const double *f, double *out, void *stream);
+
+/* surface rows (vertex/edge/face primitives) as sums of one-sided
+ * partial stencils over the incident macro elements, plus Dirichlet
+ * identity rows (0 for residuals). */
+int hhg_surface_apply(const hhg_grid *g, const hhg_surface *s, int variant,
+                      int flags, const double *u, const double *f,
+                      double *out, void *stream);
+
+/* ---------------------------------------------------------------------
+ * vector kernels (CG / multigrid plumbing)
+ * --------------------------------------------------------------------- */
+/* result[0] = sum_i x[i]*y[i] (deterministic two-pass reduction);
+ * work must hold >= 1024 doubles */
+int hhg_dot(int64_t n, const double *x, const double *y, double *work,
+            double *result, void *stream);
+/* y = a*x + y with a read from device memory: a = sign * num[0]/den[0] */
+int hhg_axpy_ratio(int64_t n, const double *num, const double *den,
+                   double sign, const double *x, double *y, void *stream);
+/* p = r + (num/den) p */
+int hhg_xpay_ratio(int64_t n, const double *num, const double *den,
+                   const double *r, double *p, void *stream);
+
+/* y = A x for a CSR matrix (prolongation, restriction = P^T as a CSR of
+ * the transpose); rows accumulate in stored column order (bitwise scipy) */
+int hhg_csr_spmv(int64_t nrows, const int64_t *indptr, const int64_t *indices,
+                 const double *data, const double *x, double *y, int accumulate,
+                 void *stream);
+
+/* y[ids[e]] = 0 (coarse Dirichlet rows after restriction) */
+int hhg_scatter_zero(int64_t n, const int64_t *ids, double *y, void *stream);
+
+/* smoother pieces (Operator.smooth): one level of the level-scheduled
+ * surface Gauss-Seidel (rows given as indices into s->rows), and the volume
+ * hyperplane wavefronts of all macro elements (reads the ghost layer, which
+ * must be refreshed after the surface sweep) */
+int hhg_smooth_surface_level(const hhg_grid *g, const hhg_surface *s,
+                             const int64_t *level_rows, int64_t count,
+                             double omega, double *u, const double *f,
+                             void *stream);
+int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef,
+                      double omega, double *u, const double *f, void *stream);
+
+/* HOST helper: level schedule of the surface Gauss-Seidel (see .cu) */
+int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr,
+                       const int64_t *dep_idx, int64_t *level);
+
+/* rows of one volume tile (W*B) the kernels were compiled with */
+int hhg_volume_tile_rows(void);
+
+/* status word of the last GS launch (HHG_OK / HHG_ERR_ZERO_DIAG) — call
+ * after synchronising the stream */
+int hhg_status(void);
+int hhg_status_reset(void);
+
+/* compile-time kernel configuration, for reports */
+const char *hhg_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HHG_B200_H */

@@ -1,0 +1,119 @@
+"""ctypes binding of libhhg_b200.so (the C ABI declared in include/hhg_b200.h).
+
+The library is built in-tree by `__graft_entry__.build()` (nvcc, sm_100a).
+There is no fallback: if the shared object is missing, or no CUDA device is
+present when a device operation is requested, the call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+__all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "check", "HhgError",
+           "VAR", "FLAG_RESIDUAL", "FLAG_FAST", "EXPORTS"]
+
+LIB_PATH = Path(__file__).resolve().parent / "libhhg_b200.so"
+
+HHG_OK, HHG_ERR_ARG, HHG_ERR_CUDA, HHG_ERR_ZERO_DIAG, HHG_ERR_TABLE = 0, -1, -2, -3, -4
+VAR = {"scaling": 0, "nodal": 1, "const": 2, "stored": 3}
+FLAG_RESIDUAL, FLAG_FAST = 1, 2
+
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+vp = ctypes.c_void_p
+
+
+class HhgError(RuntimeError):
+    pass
+
+
+class HhgGrid(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("ntets", ctypes.c_int32),
+                ("lat_size", ctypes.c_int64), ("nvol", ctypes.c_int64),
+                ("shell_size", ctypes.c_int64), ("n_nodes", ctypes.c_int64),
+                ("vol_start", vp), ("srow", vp), ("shell_gid", vp),
+                ("ghost", vp), ("kc", vp), ("tiles", vp),
+                ("ntiles", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+
+
+class HhgSurface(ctypes.Structure):
+    _fields_ = [("nrows", ctypes.c_int64), ("rows", vp), ("row_nodal", vp),
+                ("inc_ptr", vp), ("inc_tet", vp), ("inc_code", vp),
+                ("inc_cls", vp), ("psh", vp), ("pfac", vp),
+                ("ndir", ctypes.c_int64), ("dir_ids", vp)]
+
+
+# name -> (restype, argtypes); every symbol of include/hhg_b200.h
+EXPORTS = {
+    "hhg_apply_scaling_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp]),
+    "hhg_apply_nodal_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, c_i64p,
+                                          ctypes.c_int64, c_i64p, vp, c_i64p,
+                                          c_i64p, vp, vp]),
+    "hhg_apply_const_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp,
+                                          ctypes.c_double, vp, vp]),
+    "hhg_apply_stored_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),
+    "hhg_gs_scaling_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp,
+                                         ctypes.c_double, vp]),
+    "hhg_gs_nodal_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, c_i64p,
+                                       ctypes.c_int64, c_i64p, vp, c_i64p, c_i64p,
+                                       ctypes.c_double, vp]),
+    "hhg_ghost_update": (ctypes.c_int, [ctypes.POINTER(HhgGrid), vp, vp]),
+    "hhg_volume_apply": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int,
+                                        ctypes.c_int, vp, vp, vp, vp, vp, vp]),
+    "hhg_surface_apply": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                         ctypes.POINTER(HhgSurface), ctypes.c_int,
+                                         ctypes.c_int, vp, vp, vp, vp]),
+    "hhg_smooth_surface_level": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                                ctypes.POINTER(HhgSurface), vp,
+                                                ctypes.c_int64, ctypes.c_double,
+                                                vp, vp, vp]),
+    "hhg_smooth_volume": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int, vp,
+                                         ctypes.c_double, vp, vp, vp]),
+    "hhg_dot": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),
+    "hhg_axpy_ratio": (ctypes.c_int, [ctypes.c_int64, vp, vp, ctypes.c_double, vp,
+                                      vp, vp]),
+    "hhg_xpay_ratio": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),
+    "hhg_csr_spmv": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp,
+                                    ctypes.c_int, vp]),
+    "hhg_scatter_zero": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp]),
+    "hhg_status": (ctypes.c_int, []),
+    "hhg_status_reset": (ctypes.c_int, []),
+    "hhg_build_info": (ctypes.c_char_p, []),
+    "hhg_volume_tile_rows": (ctypes.c_int, []),
+    "hhg_host_gs_levels": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp]),
+}
+
+
+def _load():
+    if not LIB_PATH.exists():
+        raise HhgError(
+            f"{LIB_PATH.name} is not built; run `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (nvcc sm_100a). There is no CPU fallback.")
+    handle = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_LOCAL | ctypes.RTLD_GLOBAL * 0)
+    for name, (res, args) in EXPORTS.items():
+        fn = getattr(handle, name)
+        fn.restype = res
+        fn.argtypes = args
+    return handle
+
+
+class _Lazy:
+    _h = None
+
+    def __getattr__(self, name):
+        if _Lazy._h is None:
+            _Lazy._h = _load()
+        return getattr(_Lazy._h, name)
+
+
+lib = _Lazy()
+
+
+def check(rc, what=""):
+    if rc == HHG_OK:
+        return
+    if rc == HHG_ERR_ZERO_DIAG:
+        raise ValueError("zero central stencil entry")
+    if rc == HHG_ERR_TABLE:
+        raise ValueError(f"{what}: patch tables differ from the compiled ones")
+    raise HhgError(f"{what} failed with code {rc}")

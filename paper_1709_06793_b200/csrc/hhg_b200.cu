@@ -1,0 +1,401 @@
+// libhhg_b200: extern "C" entry points (include/hhg_b200.h) over the sm_100a
+// kernels in hhg_volume.cuh / hhg_surface.cuh / hhg_smooth.cuh.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/hhg_b200.h"
+#include "hhg_common.cuh"
+#include "hhg_smooth.cuh"
+#include "hhg_surface.cuh"
+#include "hhg_volume.cuh"
+
+using namespace hhg;
+
+#ifndef HHG_VOL_B
+#define HHG_VOL_B 2
+#endif
+#ifndef HHG_VOL_W
+#define HHG_VOL_W 8
+#endif
+#ifndef HHG_VOL_NS
+#define HHG_VOL_NS 6
+#endif
+
+static constexpr int kB = HHG_VOL_B, kW = HHG_VOL_W, kNS = HHG_VOL_NS;
+
+static inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+static inline int check(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "hhg_b200: %s: %s\n", what, cudaGetErrorString(e));
+    return HHG_ERR_CUDA;
+  }
+  return HHG_OK;
+}
+
+// ---------------------------------------------------------------------------
+// volume kernel dispatch
+// ---------------------------------------------------------------------------
+template <int VAR, int SRC, bool RES, bool FAST>
+static int launch_volume(const VolDesc &D, cudaStream_t st) {
+  if (D.ntiles <= 0) return HHG_OK;
+  constexpr int ROWS = kW * kB + 2;
+  const size_t smem = sizeof(double2) * kNS * ROWS * VOL_COLS + 72 * sizeof(double);
+  auto kern = volume_kernel<VAR, SRC, RES, FAST, kB, kW, kNS>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  kern<<<D.ntiles, 32 * kW, smem, st>>>(D);
+  return check("volume_kernel");
+}
+
+template <int SRC>
+static int dispatch_volume(const VolDesc &D, int variant, int flags, cudaStream_t st) {
+  const bool res = flags & HHG_FLAG_RESIDUAL;
+  const bool fast = flags & HHG_FLAG_FAST;
+  switch (variant) {
+    case HHG_VAR_SCALING:
+      if (fast) return res ? launch_volume<0, SRC, true, true>(D, st)
+                           : launch_volume<0, SRC, false, true>(D, st);
+      return res ? launch_volume<0, SRC, true, false>(D, st)
+                 : launch_volume<0, SRC, false, false>(D, st);
+    case HHG_VAR_NODAL:
+      return res ? launch_volume<1, SRC, true, false>(D, st)
+                 : launch_volume<1, SRC, false, false>(D, st);
+    case HHG_VAR_CONST:
+      return res ? launch_volume<2, SRC, true, false>(D, st)
+                 : launch_volume<2, SRC, false, false>(D, st);
+    case HHG_VAR_STORED:
+      return res ? launch_volume<3, SRC, true, false>(D, st)
+                 : launch_volume<3, SRC, false, false>(D, st);
+  }
+  return HHG_ERR_ARG;
+}
+
+// tiles of one macro element: 32 i-columns x (W*B) j-rows, k-march up to
+// kmax; longest first for load balance
+static std::vector<int4> make_tiles(int n, int ntets) {
+  std::vector<int4> tl;
+  const int TJ = kW * kB;
+  for (int t = 0; t < ntets; ++t)
+    for (int j0 = 1; j0 <= n - 3; j0 += TJ)
+      for (int i0 = 1; i0 + j0 <= n - 2; i0 += 32)
+        tl.push_back(make_int4(t, i0, j0, n - 1 - i0 - j0));
+  std::stable_sort(tl.begin(), tl.end(),
+                   [](const int4 &a, const int4 &b) { return a.w > b.w; });
+  return tl;
+}
+
+// per-element ABI: one macro element, lattice layout (tiles cached per n)
+struct ElemTiles {
+  int n = -1;
+  int4 *dev = nullptr;
+  int count = 0;
+};
+static ElemTiles g_elem_tiles;
+
+static int elem_tiles(int n, const int4 **tiles, int *count) {
+  if (g_elem_tiles.n != n) {
+    std::vector<int4> tl = make_tiles(n, 1);
+    if (g_elem_tiles.dev) cudaFree(g_elem_tiles.dev);
+    g_elem_tiles.dev = nullptr;
+    if (!tl.empty()) {
+      if (cudaMalloc(&g_elem_tiles.dev, tl.size() * sizeof(int4)) != cudaSuccess)
+        return HHG_ERR_CUDA;
+      cudaMemcpy(g_elem_tiles.dev, tl.data(), tl.size() * sizeof(int4),
+                 cudaMemcpyHostToDevice);
+    }
+    g_elem_tiles.n = n;
+    g_elem_tiles.count = (int)tl.size();
+  }
+  *tiles = g_elem_tiles.dev;
+  *count = g_elem_tiles.count;
+  return HHG_OK;
+}
+
+static VolDesc elem_desc(int64_t n, const double *v, const double *kc,
+                         const double *coef, int stride, double *out) {
+  VolDesc D{};
+  D.n = (int)n;
+  D.ntets = 1;
+  D.L = tetra(n);
+  D.nvol = n >= 4 ? tetra(n - 4) : 0;
+  D.kc = kc;
+  D.u = v;
+  D.out = out;
+  D.coef = coef;
+  D.coef_stride = stride;
+  return D;
+}
+
+static bool tables_match(const int64_t *sched, int64_t nsched, const int64_t *sums,
+                         const int64_t *tptr, const int64_t *telem) {
+  if (nsched != 40) return false;
+  for (int r = 0; r < 40; ++r)
+    for (int c = 0; c < 3; ++c)
+      if (sched[r * 3 + c] != pt_cse(r, c)) return false;
+  for (int e = 0; e < 24; ++e)
+    if (sums[e] != 31 + e) return false;
+  for (int d = 0; d < 15; ++d)
+    if (tptr[d] != pt_tptr(d)) return false;
+  for (int t = 0; t < 72; ++t)
+    if (telem[t] != pt_telem(t)) return false;
+  return true;
+}
+
+extern "C" {
+
+int hhg_apply_scaling_3d(int64_t n, const int64_t *, const double *v, const double *kc,
+                         const double *sh, double *out, void *stream) {
+  if (n < 4) return HHG_OK;
+  VolDesc D = elem_desc(n, v, kc, sh, 14, out);
+  int rc = elem_tiles((int)n, &D.tiles, &D.ntiles);
+  if (rc) return rc;
+  return dispatch_volume<SRC_LATTICE>(D, HHG_VAR_SCALING, 0, S(stream));
+}
+
+int hhg_apply_nodal_3d(int64_t n, const int64_t *, const double *v, const double *kc,
+                       const int64_t *sched, int64_t nsched, const int64_t *sums,
+                       const double *fac, const int64_t *tptr, const int64_t *telem,
+                       double *out, void *stream) {
+  if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
+  if (n < 4) return HHG_OK;
+  VolDesc D = elem_desc(n, v, kc, fac, 72, out);
+  int rc = elem_tiles((int)n, &D.tiles, &D.ntiles);
+  if (rc) return rc;
+  return dispatch_volume<SRC_LATTICE>(D, HHG_VAR_NODAL, 0, S(stream));
+}
+
+int hhg_apply_const_3d(int64_t n, const int64_t *, const double *v, const double *s15,
+                       double, double *out, void *stream) {
+  // s15: 14 neighbour weights followed by c0 (device); the c0 argument is
+  // accepted for signature parity and must equal s15[14]
+  if (n < 4) return HHG_OK;
+  VolDesc D = elem_desc(n, v, v, s15, 15, out);
+  int rc = elem_tiles((int)n, &D.tiles, &D.ntiles);
+  if (rc) return rc;
+  return dispatch_volume<SRC_LATTICE>(D, HHG_VAR_CONST, 0, S(stream));
+}
+
+int hhg_apply_stored_3d(int64_t n, const int64_t *, const double *v, const double *w,
+                        double *out, void *stream) {
+  if (n < 4) return HHG_OK;
+  VolDesc D = elem_desc(n, v, v, nullptr, 0, out);
+  D.w = w;
+  int rc = elem_tiles((int)n, &D.tiles, &D.ntiles);
+  if (rc) return rc;
+  return dispatch_volume<SRC_LATTICE>(D, HHG_VAR_STORED, 0, S(stream));
+}
+
+static int gs_elem(int var, int64_t n, double *u, const double *fv, const double *kc,
+                   const double *coef, int stride, double omega, cudaStream_t st) {
+  if (n < 4) return HHG_OK;
+  GSDesc G{};
+  G.n = (int)n;
+  G.ntets = 1;
+  G.L = tetra(n);
+  G.nvol = tetra(n - 4);
+  G.kc = kc;
+  G.u = u;
+  G.f = fv;
+  G.coef = coef;
+  G.coef_stride = stride;
+  G.omega = omega;
+  G.lattice = 1;
+  if (var == 0) gs_volume_kernel<0><<<1, 1024, 0, st>>>(G);
+  else gs_volume_kernel<1><<<1, 1024, 0, st>>>(G);
+  return check("gs_volume_kernel");
+}
+
+int hhg_gs_scaling_3d(int64_t n, const int64_t *, double *u, const double *fv,
+                      const double *kc, const double *sh, double omega, void *stream) {
+  return gs_elem(0, n, u, fv, kc, sh, 14, omega, S(stream));
+}
+
+int hhg_gs_nodal_3d(int64_t n, const int64_t *, double *u, const double *fv,
+                    const double *kc, const int64_t *sched, int64_t nsched,
+                    const int64_t *sums, const double *fac, const int64_t *tptr,
+                    const int64_t *telem, double omega, void *stream) {
+  if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
+  return gs_elem(1, n, u, fv, kc, fac, 72, omega, S(stream));
+}
+
+// ---------------------------------------------------------------------------
+// batched operator entry points
+// ---------------------------------------------------------------------------
+static VolDesc grid_desc(const hhg_grid *g) {
+  VolDesc D{};
+  D.n = g->n;
+  D.ntets = g->ntets;
+  D.L = g->lat_size;
+  D.nvol = g->nvol;
+  D.S = g->shell_size;
+  D.vol_start = reinterpret_cast<const long long *>(g->vol_start);
+  D.srow = g->srow;
+  D.ghost = g->ghost;
+  D.kc = g->kc;
+  D.tiles = reinterpret_cast<const int4 *>(g->tiles);
+  D.ntiles = g->ntiles;
+  return D;
+}
+
+int hhg_ghost_update(const hhg_grid *g, const double *u, void *stream) {
+  const long long total = (long long)g->ntets * g->shell_size;
+  if (total == 0) return HHG_OK;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  ghost_kernel<<<blocks, 256, 0, S(stream)>>>(
+      total, reinterpret_cast<const long long *>(g->shell_gid), u, g->ghost);
+  return check("ghost_kernel");
+}
+
+int hhg_volume_apply(const hhg_grid *g, int variant, int flags, const double *coef,
+                     const double *w, const double *u, const double *f, double *out,
+                     void *stream) {
+  if (g->n < 4 || g->ntiles == 0) return HHG_OK;
+  VolDesc D = grid_desc(g);
+  D.u = u;
+  D.f = f;
+  D.out = out;
+  D.coef = coef;
+  D.coef_stride = variant == HHG_VAR_NODAL ? 72 : (variant == HHG_VAR_CONST ? 15 : 14);
+  D.w = w;
+  return dispatch_volume<SRC_SPLIT>(D, variant, flags, S(stream));
+}
+
+static SurfDesc surf_desc(const hhg_grid *g, const hhg_surface *s) {
+  SurfDesc D{};
+  D.n = g->n;
+  D.L = g->lat_size;
+  D.S = g->shell_size;
+  D.nrows = s->nrows;
+  D.vol_start = reinterpret_cast<const long long *>(g->vol_start);
+  D.srow = g->srow;
+  D.ghost = g->ghost;
+  D.kc = g->kc;
+  D.rows = reinterpret_cast<const long long *>(s->rows);
+  D.row_nodal = s->row_nodal;
+  D.inc_ptr = s->inc_ptr;
+  D.inc_tet = s->inc_tet;
+  D.inc_code = s->inc_code;
+  D.inc_cls = s->inc_cls;
+  D.psh = s->psh;
+  D.pfac = s->pfac;
+  return D;
+}
+
+int hhg_surface_apply(const hhg_grid *g, const hhg_surface *s, int, int flags,
+                      const double *u, const double *f, double *out, void *stream) {
+  const bool res = flags & HHG_FLAG_RESIDUAL;
+  SurfDesc D = surf_desc(g, s);
+  D.u = u;
+  D.f = f;
+  D.out = out;
+  if (s->nrows > 0) {
+    const int blocks = (int)((s->nrows + 127) / 128);
+    if (res) surface_kernel<true><<<blocks, 128, 0, S(stream)>>>(D);
+    else surface_kernel<false><<<blocks, 128, 0, S(stream)>>>(D);
+    int rc = check("surface_kernel");
+    if (rc) return rc;
+  }
+  if (s->ndir > 0) {
+    const int blocks = (int)((s->ndir + 255) / 256);
+    const long long *ids = reinterpret_cast<const long long *>(s->dir_ids);
+    if (res) dirichlet_kernel<true><<<blocks, 256, 0, S(stream)>>>(s->ndir, ids, u, out);
+    else dirichlet_kernel<false><<<blocks, 256, 0, S(stream)>>>(s->ndir, ids, u, out);
+    return check("dirichlet_kernel");
+  }
+  return HHG_OK;
+}
+
+// smoother: surface rows level by level, then refresh the ghost layer, then
+// the volume wavefronts of all macro elements (one CTA each)
+int hhg_smooth_surface_level(const hhg_grid *g, const hhg_surface *s,
+                             const int64_t *level_rows, int64_t count, double omega,
+                             double *u, const double *f, void *stream) {
+  if (count <= 0) return HHG_OK;
+  SurfGSDesc G{};
+  G.s = surf_desc(g, s);
+  G.s.u = u;
+  G.s.f = f;
+  G.shell_gid = reinterpret_cast<const long long *>(g->shell_gid);
+  G.level_rows = reinterpret_cast<const long long *>(level_rows);
+  G.count = count;
+  G.omega = omega;
+  gs_surface_kernel<<<(int)((count + 127) / 128), 128, 0, S(stream)>>>(G);
+  return check("gs_surface_kernel");
+}
+
+int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double omega,
+                      double *u, const double *f, void *stream) {
+  if (g->n < 4) return HHG_OK;
+  GSDesc G{};
+  G.n = g->n;
+  G.ntets = g->ntets;
+  G.L = g->lat_size;
+  G.S = g->shell_size;
+  G.nvol = g->nvol;
+  G.vol_start = reinterpret_cast<const long long *>(g->vol_start);
+  G.srow = g->srow;
+  G.ghost = g->ghost;
+  G.kc = g->kc;
+  G.u = u;
+  G.f = f;
+  G.coef = coef;
+  G.coef_stride = variant == HHG_VAR_NODAL ? 72 : 14;
+  G.omega = omega;
+  G.lattice = 0;
+  if (variant == HHG_VAR_NODAL) gs_volume_kernel<1><<<g->ntets, 1024, 0, S(stream)>>>(G);
+  else gs_volume_kernel<0><<<g->ntets, 1024, 0, S(stream)>>>(G);
+  return check("gs_volume_kernel");
+}
+
+int hhg_status(void) {
+  int v = 0;
+  cudaMemcpyFromSymbol(&v, g_status, sizeof(int));
+  return v ? HHG_ERR_ZERO_DIAG : HHG_OK;
+}
+
+int hhg_status_reset(void) {
+  int z = 0;
+  cudaMemcpyToSymbol(g_status, &z, sizeof(int));
+  return HHG_OK;
+}
+
+int hhg_volume_tile_rows(void) { return kW * kB; }
+
+// host-side level schedule of the surface Gauss-Seidel: rows are in
+// ascending global id, dep_idx[dep_ptr[r]..dep_ptr[r+1]) lists the row
+// indices q < r row r reads updated values from.  level[r] = 1 + max level[q]
+// in one ascending pass (O(nnz)).  Returns the number of levels.
+int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr, const int64_t *dep_idx,
+                       int64_t *level) {
+  int64_t nlev = 0;
+  for (int64_t r = 0; r < nrows; ++r) {
+    int64_t lv = 0;
+    for (int64_t e = dep_ptr[r]; e < dep_ptr[r + 1]; ++e) {
+      const int64_t q = dep_idx[e];
+      if (q >= r) return HHG_ERR_ARG;
+      if (level[q] + 1 > lv) lv = level[q] + 1;
+    }
+    level[r] = lv;
+    if (lv + 1 > nlev) nlev = lv + 1;
+  }
+  return (int)nlev;
+}
+
+const char *hhg_build_info(void) {
+  static char buf[128];
+  snprintf(buf, sizeof buf, "sm_100a volume B=%d W=%d NS=%d", kB, kW, kNS);
+  return buf;
+}
+
+}  // extern "C"
+
+#include "hhg_vector.cuh"

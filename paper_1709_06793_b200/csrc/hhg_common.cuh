@@ -1,0 +1,128 @@
+// Shared device helpers: lattice arithmetic, patch tables, fp64 ops.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hhg {
+
+// ---------------------------------------------------------------------------
+// lattice arithmetic (mesh.py: SimplexLattice, closed form of base[k, j])
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ long long tetra(long long m) {
+  // points of a size-m tetrahedral lattice, 0 for m < 0
+  return m < 0 ? 0 : (m + 1) * (m + 2) * (m + 3) / 6;
+}
+__host__ __device__ __forceinline__ long long lbase(int n, int k, int j) {
+  return tetra(n) - tetra(n - k) + (long long)j * (n + 1 - k) -
+         (long long)j * (j - 1) / 2;
+}
+
+// the 14 stencil directions (di, dj, dk), mesh.py:44-48
+__constant__ int8_t c_dirs[14][3] = {
+    {1, 0, 0},  {0, 1, 0},  {0, 0, 1},  {1, -1, 0},  {1, 0, -1},
+    {0, 1, -1}, {1, -1, 1}, {-1, 0, 0}, {0, -1, 0},  {0, 0, -1},
+    {-1, 1, 0}, {-1, 0, 1}, {0, -1, 1}, {-1, 1, -1}};
+
+// patch tables (reference_stencils.py:48-75 and Environment.term_*):
+// term t of direction d (t in [TPTR[d], TPTR[d+1])) reads element sum slot
+// 31 + TELEM[t].
+#define HHG_TPTR {0, 6, 10, 16, 22, 26, 32, 36, 42, 46, 52, 58, 62, 68, 72}
+#define HHG_TELEM                                                            \
+  {18, 19, 20, 21, 22, 23, 10, 11, 18, 20, 6,  7,  10, 14, 18, 19, 12, 13,   \
+   15, 17, 22, 23, 16, 17, 21, 23, 8,  9,  11, 16, 20, 21, 14, 15, 19, 22,   \
+   0,  1,  2,  3,  4,  5,  4,  5,  12, 13, 3,  5,  9,  13, 16, 17, 0,  2,    \
+   6,  8,  10, 11, 0,  1,  6,  7,  1,  4,  7,  12, 14, 15, 2,  3,  8,  9}
+#define HHG_CSE                                                              \
+  {{15, 0, 1},   {16, 0, 10},  {17, 0, 11},  {18, 0, 13},  {19, 8, 12},      \
+   {20, 8, 14},  {21, 8, 9},   {22, 3, 12},  {23, 6, 14},  {24, 2, 3},       \
+   {25, 2, 6},   {26, 4, 9},   {27, 3, 7},   {28, 4, 7},   {29, 5, 6},       \
+   {30, 4, 5},   {31, 17, 19}, {32, 18, 19}, {33, 17, 20}, {34, 16, 20},     \
+   {35, 18, 21}, {36, 16, 21}, {37, 17, 22}, {38, 18, 22}, {39, 17, 23},     \
+   {40, 16, 23}, {41, 17, 24}, {42, 17, 25}, {43, 18, 26}, {44, 16, 26},     \
+   {45, 18, 27}, {46, 18, 28}, {47, 16, 29}, {48, 16, 30}, {49, 15, 24},     \
+   {50, 15, 27}, {51, 15, 25}, {52, 15, 29}, {53, 15, 28}, {54, 15, 30}}
+
+// compile-time accessors (indices are constants after full unrolling)
+__host__ __device__ constexpr int pt_tptr(int d) {
+  constexpr int a[15] = HHG_TPTR;
+  return a[d];
+}
+__host__ __device__ constexpr int pt_telem(int t) {
+  constexpr int a[72] = HHG_TELEM;
+  return a[t];
+}
+__host__ __device__ constexpr int pt_cse(int r, int c) {
+  constexpr int a[40][3] = HHG_CSE;
+  return a[r][c];
+}
+
+// bitmask of stencil directions that stay inside the closed macro element
+// for each of the 14 boundary classes (reference_stencils.class_element_masks)
+__constant__ uint16_t c_cls_dirmask[14] = {16312, 4991, 11959, 7631, 4920,
+                                           11952, 567,  7560,  4431, 3207,
+                                           560,   4360, 3200,  7};
+
+// ---------------------------------------------------------------------------
+// fp64 arithmetic: the bitwise path uses explicit round-to-nearest ops so
+// nvcc cannot contract mul+add into FMA (the reference runs numba without
+// fastmath, kernels.py:10)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// scaled-stencil row, exact reference order:
+//   acc = sum_d ((k0 + kq) * sh[d]) * (vq - v0), d = 0..13 left to right
+__device__ __forceinline__ double scaling_row_exact(double v0, double k0,
+                                                    const double2 (&q)[14],
+                                                    const double (&sh)[14]) {
+  double acc = dmul(dmul(dadd(k0, q[0].y), sh[0]), dsub(q[0].x, v0));
+#pragma unroll
+  for (int d = 1; d < 14; ++d)
+    acc = dadd(acc, dmul(dmul(dadd(k0, q[d].y), sh[d]), dsub(q[d].x, v0)));
+  return acc;
+}
+
+// reassociated form: mirror pairs (d, d+7) share a folded weight, FMAs
+// (sh2[d] holds the pair weight, host checked |sh[d]-sh[d+7]| tiny)
+__device__ __forceinline__ double scaling_row_fast(double v0, double k0,
+                                                   const double2 (&q)[14],
+                                                   const double (&sh)[14]) {
+  double acc = 0.0;
+#pragma unroll
+  for (int d = 0; d < 7; ++d) {
+    double m = (k0 + q[d].y) * (q[d].x - v0);
+    m = fma(k0 + q[d + 7].y, q[d + 7].x - v0, m);
+    acc = fma(sh[d], m, acc);
+  }
+  return acc;
+}
+
+// nodal-integration row, exact reference order (kernels.py:139-189)
+template <class FAC>
+__device__ __forceinline__ double nodal_row_exact(double v0, double k0,
+                                                  const double2 (&q)[14],
+                                                  const FAC &fac) {
+  double b[55];
+  b[0] = k0;
+#pragma unroll
+  for (int d = 0; d < 14; ++d) b[1 + d] = q[d].y;
+#pragma unroll
+  for (int r = 0; r < 40; ++r)
+    b[pt_cse(r, 0)] = dadd(b[pt_cse(r, 1)], b[pt_cse(r, 2)]);
+  double acc = 0.0;
+#pragma unroll
+  for (int d = 0; d < 14; ++d) {
+    const int t0 = pt_tptr(d);
+    double s = dmul(b[31 + pt_telem(t0)], fac[t0]);
+#pragma unroll
+    for (int t = t0 + 1; t < pt_tptr(d + 1); ++t)
+      s = dadd(s, dmul(b[31 + pt_telem(t)], fac[t]));
+    const double term = dmul(s, dsub(q[d].x, v0));
+    acc = (d == 0) ? term : dadd(acc, term);
+  }
+  return acc;
+}
+
+}  // namespace hhg

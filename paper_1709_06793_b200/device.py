@@ -1,0 +1,260 @@
+"""Device-resident grid and surface tables for the batched kernels.
+
+HBM layout:
+
+* global vectors (u, f, out) stay in the reference's node numbering; the
+  interior of macro element t is the contiguous run
+  ``[vol_start[t], vol_start[t] + nvol)`` in (k, j, i) order, which is its
+  lattice interior row by row — the volume kernel streams it directly;
+* the ghost layer of t is a compact copy of its lattice shell (all points of
+  the rows with k = 0, j = 0 or k + j >= n - 1, and the two end points
+  i = 0, i = end of every other row), ``srow[k, j]`` gives a row's offset;
+  ``shell_gid`` maps shell points to global ids and is the gather list of
+  the ghost-layer update;
+* the coefficient k lives in full lattice layout per element (8 B/point).
+
+Host-side table construction is numpy; the device copies are torch tensors
+used purely as buffers.
+"""
+from __future__ import annotations
+
+import ctypes
+from functools import lru_cache
+
+import numpy as np
+
+from ._lib import HhgGrid, HhgSurface, lib
+from .mesh import SimplexLattice, lattice_size
+from .reference_stencils import CLASS_OF_MASK, class_element_masks
+from .mesh import DIRS_3D
+
+__all__ = ["shell_layout", "volume_tiles", "GridTables", "SurfaceTables",
+           "DeviceGrid", "DeviceSurface", "require_cuda"]
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the hhg_b200 operators run only on "
+                           "the GPU (there is no CPU fallback)")
+    return torch
+
+
+@lru_cache(maxsize=16)
+def shell_layout(n: int):
+    """(srow[(n+1)^2] int32, shell lattice positions int64, shell size)."""
+    lat = SimplexLattice(3, n)
+    srow = np.full((n + 1) * (n + 1), -1, dtype=np.int32)
+    pos = []
+    off = 0
+    for k in range(n + 1):
+        for j in range(n + 1 - k):
+            b = int(lat.base[k, j])
+            rl = n + 1 - k - j
+            srow[k * (n + 1) + j] = off
+            if k >= 1 and j >= 1 and k + j <= n - 2:
+                pos += [b, b + rl - 1]
+                off += 2
+            else:
+                pos += list(range(b, b + rl))
+                off += rl
+    pos = np.asarray(pos, dtype=np.int64)
+    srow.setflags(write=False)
+    pos.setflags(write=False)
+    return srow, pos, off
+
+
+def volume_tiles(n: int, ntets: int, tile_rows: int):
+    """(tet, i0, j0, kmax) work tiles, longest k-march first (stable)."""
+    tl = []
+    for j0 in range(1, n - 2, tile_rows):
+        for i0 in range(1, n - 1 - j0, 32):
+            tl.append((i0, j0, n - 1 - i0 - j0))
+    if not tl or ntets == 0:
+        return np.zeros((0, 4), dtype=np.int32)
+    base = np.array(tl, dtype=np.int32)
+    t = np.repeat(np.arange(ntets, dtype=np.int32), len(base))
+    allt = np.column_stack([t, np.tile(base, (ntets, 1))])
+    order = np.argsort(-allt[:, 3], kind="stable")
+    return np.ascontiguousarray(allt[order])
+
+
+class GridTables:
+    """Host-side (numpy) tables of one grid level on one device."""
+
+    def __init__(self, grid, tile_rows=None):
+        n = grid.n
+        self.n = n
+        self.ntets = grid.macro.n_elements
+        self.L = lattice_size(n)
+        self.nvol = grid.nodes_per_volume
+        self.n_nodes = grid.n_nodes
+        self.vol_start = np.ascontiguousarray(grid.vol_start, dtype=np.int64)
+        self.srow, self.shell_pos, self.S = shell_layout(n)
+        self.shell_gid = np.ascontiguousarray(grid.elem_gidx[:, self.shell_pos])
+        if tile_rows is None:
+            tile_rows = int(lib.hhg_volume_tile_rows())
+        self.tiles = volume_tiles(n, self.ntets, tile_rows)
+
+
+def _point_codes(lat, pos):
+    c = lat.coords[pos]
+    return (c[:, 0] | (c[:, 1] << 10) | (c[:, 2] << 20)).astype(np.int32), c
+
+
+class SurfaceTables:
+    """Incidence lists of the non-Dirichlet surface rows.
+
+    Every shell point p of every macro element t whose global node r is a
+    free surface node contributes one incidence (t, p, class(p)) to row r;
+    rows are sorted by global id and incidences by t, so row sums have a
+    fixed order.
+    """
+
+    def __init__(self, grid, gt: GridTables, nodal_kinds=frozenset()):
+        n = grid.n
+        lat = grid.lat
+        free_surface = np.zeros(grid.n_nodes, dtype=bool)
+        free_surface[:grid.n_surface_nodes] = True
+        free_surface &= ~grid.dirichlet_mask
+        code, coords = _point_codes(lat, gt.shell_pos)
+        bary = np.column_stack([n - coords.sum(axis=1), coords])
+        zmask = ((bary == 0) * (1 << np.arange(4))).sum(axis=1)
+        cls = np.array([CLASS_OF_MASK.get(int(m), 255) for m in zmask], dtype=np.uint8)
+        gid = gt.shell_gid                                   # (ntets, S)
+        keep = free_surface[gid]
+        tet = np.broadcast_to(np.arange(gt.ntets, dtype=np.int32)[:, None], gid.shape)
+        g = gid[keep]
+        order = np.lexsort((tet[keep], g))                   # by gid, then tet
+        g = g[order]
+        self.inc_tet = np.ascontiguousarray(tet[keep][order])
+        spos = np.broadcast_to(np.arange(gt.S)[None, :], gid.shape)[keep][order]
+        self.inc_code = np.ascontiguousarray(code[spos])
+        self.inc_cls = np.ascontiguousarray(cls[spos])
+        self.inc_spos = spos
+        if (self.inc_cls == 255).any():
+            raise AssertionError("interior lattice point listed as a shell incidence")
+        self.rows, first = np.unique(g, return_index=True)
+        self.inc_ptr = np.append(first, len(g)).astype(np.int32)
+        kinds = grid.node_kind[self.rows]
+        self.row_nodal = np.isin(kinds, [int(k) for k in nodal_kinds]).astype(np.uint8)
+        self.dir_ids = np.nonzero(grid.dirichlet_mask)[0].astype(np.int64)
+        self._grid = grid
+        self._gt = gt
+
+    def neighbour_gids(self):
+        """(ninc, 14) global ids of each incidence's in-element neighbours
+        (-1 for directions leaving the macro element)."""
+        gt, grid = self._gt, self._grid
+        lat = grid.lat
+        n = gt.n
+        i = self.inc_code & 1023
+        j = (self.inc_code >> 10) & 1023
+        k = (self.inc_code >> 20) & 1023
+        _, dir_inside = class_element_masks()
+        out = np.full((len(i), 14), -1, dtype=np.int64)
+        for d, (di, dj, dk) in enumerate(DIRS_3D):
+            ok = dir_inside[self.inc_cls, d]
+            qi, qj, qk = i[ok] + di, j[ok] + dj, k[ok] + dk
+            flat = lat.base[qk, qj] + qi
+            out[ok, d] = grid.elem_gidx[self.inc_tet[ok], flat]
+        return out
+
+    def gs_levels(self):
+        """Level schedule of the forward surface GS (ascending-id order)."""
+        nb = self.neighbour_gids()
+        rows = self.rows
+        nrows = len(rows)
+        row_of_inc = np.repeat(np.arange(nrows), np.diff(self.inc_ptr))
+        pos = np.searchsorted(rows, nb)
+        pos_c = np.minimum(pos, nrows - 1)
+        is_row = (nb >= 0) & (rows[pos_c] == nb)
+        dep_row = np.where(is_row, pos_c, -1)
+        src = np.repeat(row_of_inc, 14).reshape(-1, 14)
+        m = (dep_row >= 0) & (dep_row < src)
+        pairs = np.unique(np.column_stack([src[m], dep_row[m]]), axis=0)
+        dep_ptr = np.searchsorted(pairs[:, 0], np.arange(nrows + 1)).astype(np.int64)
+        dep_idx = np.ascontiguousarray(pairs[:, 1], dtype=np.int64)
+        level = np.zeros(nrows, dtype=np.int64)
+        nlev = lib.hhg_host_gs_levels(
+            nrows, dep_ptr.ctypes.data, dep_idx.ctypes.data, level.ctypes.data)
+        if nlev < 0:
+            raise AssertionError("surface dependency list is not lower triangular")
+        order = np.argsort(level, kind="stable")
+        level_ptr = np.searchsorted(level[order], np.arange(nlev + 1))
+        return order.astype(np.int64), level_ptr.astype(np.int64), int(nlev)
+
+
+def partial_tables(op_tables):
+    """Stack per-element partial stencils (psh, pfac)."""
+    psh = np.ascontiguousarray(np.stack([p for p, _ in op_tables]))
+    pfac = np.ascontiguousarray(np.stack([f for _, f in op_tables]))
+    return psh, pfac
+
+
+class DeviceGrid:
+    """Torch buffers + the hhg_grid descriptor of one level."""
+
+    def __init__(self, gt: GridTables, kc_values: np.ndarray):
+        torch = require_cuda()
+        dev = torch.device("cuda")
+        self.gt = gt
+        t = lambda a, dt=None: torch.as_tensor(np.ascontiguousarray(a), device=dev) \
+            if dt is None else torch.as_tensor(np.ascontiguousarray(a, dtype=dt), device=dev)
+        self.vol_start = t(gt.vol_start)
+        self.srow = t(gt.srow)
+        self.shell_gid = t(gt.shell_gid)
+        self.ghost = torch.zeros(gt.ntets * gt.S, dtype=torch.float64, device=dev)
+        self.kc = t(kc_values, np.float64).reshape(-1)
+        self.tiles = t(gt.tiles)
+        d = HhgGrid()
+        d.n, d.ntets = gt.n, gt.ntets
+        d.lat_size, d.nvol, d.shell_size, d.n_nodes = gt.L, gt.nvol, gt.S, gt.n_nodes
+        d.vol_start = self.vol_start.data_ptr()
+        d.srow = self.srow.data_ptr()
+        d.shell_gid = self.shell_gid.data_ptr()
+        d.ghost = self.ghost.data_ptr()
+        d.kc = self.kc.data_ptr()
+        d.tiles = self.tiles.data_ptr() if len(gt.tiles) else None
+        d.ntiles = len(gt.tiles)
+        self.desc = d
+        self.ref = ctypes.byref(d)
+
+
+class DeviceSurface:
+    def __init__(self, st: SurfaceTables, psh, pfac):
+        torch = require_cuda()
+        dev = torch.device("cuda")
+        t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
+        self.st = st
+        self.rows = t(st.rows)
+        self.row_nodal = t(st.row_nodal)
+        self.inc_ptr = t(st.inc_ptr)
+        self.inc_tet = t(st.inc_tet)
+        self.inc_code = t(st.inc_code)
+        self.inc_cls = t(st.inc_cls)
+        self.psh = t(psh)
+        self.pfac = t(pfac) if pfac is not None else None
+        self.dir_ids = t(st.dir_ids)
+        d = HhgSurface()
+        d.nrows = len(st.rows)
+        d.rows = self.rows.data_ptr()
+        d.row_nodal = self.row_nodal.data_ptr()
+        d.inc_ptr = self.inc_ptr.data_ptr()
+        d.inc_tet = self.inc_tet.data_ptr()
+        d.inc_code = self.inc_code.data_ptr()
+        d.inc_cls = self.inc_cls.data_ptr()
+        d.psh = self.psh.data_ptr()
+        d.pfac = self.pfac.data_ptr() if self.pfac is not None else None
+        d.ndir = len(st.dir_ids)
+        d.dir_ids = self.dir_ids.data_ptr()
+        self.desc = d
+        self.ref = ctypes.byref(d)
+        self._levels = None
+
+    def levels(self):
+        if self._levels is None:
+            torch = require_cuda()
+            order, ptr, nlev = self.st.gs_levels()
+            self._levels = (torch.as_tensor(order, device="cuda"), ptr, nlev)
+        return self._levels

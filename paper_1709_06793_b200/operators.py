@@ -1,0 +1,338 @@
+"""Drop-in `Operator` with the reference signature, executed on the B200.
+
+Mirrors `pkg/src/hhgscale/operators.py:142-561`:
+
+    Operator(grid, variant, coeff=None, hybrid_nodal=frozenset())
+    .apply(u) -> A u              (Dirichlet rows: identity)
+    .residual(u, f) -> f - A u    (Dirichlet rows: 0)
+    .smooth(u, f, sweeps=1, omega=1.0)   forward Gauss-Seidel in global order
+    .stencil_weights(t), .store_stencils()
+    .flops_add / .flops_mul       analytic counters (costmodel.py:36-55)
+
+Inputs may be numpy arrays (copied to the device and back, the reference
+contract) or CUDA float64 torch tensors (device-resident, no copies).  Volume
+rows run through the batched sm_100a stencil kernels; surface rows through
+the matrix-free partial-stencil kernel; there is no host arithmetic on any
+apply, residual or smoothing path.
+"""
+from __future__ import annotations
+
+import warnings
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+from .coefficients import CoefficientField
+from .costmodel import analytic_count
+from .device import (DeviceGrid, DeviceSurface, GridTables, SurfaceTables,
+                     require_cuda)
+from .mesh import PrimitiveKind
+from .reference_stencils import (classify_edge_types, environment,
+                                 nodal_factors, partial_stencils,
+                                 reference_stencil)
+
+__all__ = ["Operator", "VARIANTS", "parse_hybrid_set"]
+
+VARIANTS = ("const", "nodal", "scaling", "scaling_ma2", "hybrid", "stored")
+
+_KIND_NAMES = {"wv": PrimitiveKind.VERTEX, "we": PrimitiveKind.EDGE,
+               "wf": PrimitiveKind.FACE}
+
+
+def parse_hybrid_set(spec: str):
+    """'wv+we' style row-class spec -> frozenset of PrimitiveKind."""
+    s = spec.strip().lower()
+    if s in ("w", "all"):
+        return frozenset(_KIND_NAMES.values())
+    if not s:
+        return frozenset()
+    out = set()
+    for tok in s.replace(",", "+").split("+"):
+        if tok not in _KIND_NAMES:
+            raise ValueError(f"unknown primitive class {tok!r} in {spec!r}")
+        out.add(_KIND_NAMES[tok])
+    return frozenset(out)
+
+
+class Operator:
+    """One operator variant bound to a grid and coefficient, on the GPU."""
+
+    def __init__(self, grid, variant: str, coeff=None, hybrid_nodal=frozenset(),
+                 fast=False):
+        if variant not in VARIANTS:
+            raise ValueError(f"unknown variant {variant!r}")
+        if variant == "stored":
+            raise ValueError("build the stored variant via store_stencils()")
+        self.grid = grid
+        self.variant = variant
+        self.coeff = coeff
+        self.hybrid_nodal = frozenset(hybrid_nodal)
+        self.dim = grid.dim
+        self.is_tensor = False
+        self.flops_add = 0
+        self.flops_mul = 0
+        self.ma2_marked = None
+        self._stored = None
+        self.fast = bool(fast)
+        if variant == "const":
+            self.const_value = 1.0 if coeff is None else float(coeff)
+            if self.const_value <= 0:
+                raise ValueError("constant coefficient must be positive")
+        else:
+            if not isinstance(coeff, CoefficientField) and not (
+                    hasattr(coeff, "values") and hasattr(coeff, "grid")):
+                raise ValueError("variant needs a sampled coefficient field")
+            if coeff.grid is not grid:
+                raise ValueError("coefficient sampled on a different grid")
+        if grid.dim != 3:
+            raise ValueError("the B200 operators are tetrahedral (dim 3)")
+        self._env = environment(3)
+        self._nvol = grid.nodes_per_volume
+        self._setup_tables()
+        self._dev = None
+
+    # -- host setup (tables only; no operator arithmetic) --------------------
+    def _setup_tables(self):
+        grid = self.grid
+        ne = grid.macro.n_elements
+        self._sh, self._fac = [], []
+        if self.variant == "scaling_ma2":
+            self._warn_3d_safeguard()
+        for t in range(ne):
+            _, s = reference_stencil(grid, t)
+            self._sh.append(s / 2.0)
+            self._fac.append(nodal_factors(grid, t) if self.variant == "nodal" else None)
+        parts = [partial_stencils(grid, t) for t in range(ne)]
+        self._psh = np.ascontiguousarray(np.stack([p for p, _ in parts])) if ne else \
+            np.zeros((0, 14, 14))
+        need_fac = self.variant in ("nodal", "hybrid")
+        self._pfac = np.ascontiguousarray(np.stack([f for _, f in parts])) \
+            if (need_fac and ne) else None
+        if self.variant == "const":
+            # element rows c * A_hat == scaling rows with k == c
+            coef = []
+            for t in range(ne):
+                s = self.const_value * 2.0 * self._sh[t]
+                coef.append(np.append(s, -s.sum()))
+            self._coef = np.ascontiguousarray(np.stack(coef)) if ne else np.zeros((0, 15))
+        elif self.variant == "nodal":
+            self._coef = np.ascontiguousarray(np.stack(self._fac)) if ne else np.zeros((0, 72))
+        else:
+            self._coef = np.ascontiguousarray(np.stack(self._sh)) if ne else np.zeros((0, 14))
+        if self.variant == "nodal":
+            self._nodal_kinds = frozenset(PrimitiveKind)
+        elif self.variant == "hybrid":
+            self._nodal_kinds = self.hybrid_nodal
+        else:
+            self._nodal_kinds = frozenset()
+
+    def _warn_3d_safeguard(self):
+        """3-D MA2 is a diagnostic only (operators.py:257-275)."""
+        grid = self.grid
+        hits = []
+        for t in range(grid.macro.n_elements):
+            _, s, _ = classify_edge_types(grid, t)
+            if not np.any(s > 0):
+                continue
+            kv = self.coeff.values[t]
+            if kv.max() / kv.min() > 2.0:
+                hits.append(t)
+        if hits:
+            warnings.warn(
+                "3D safeguard not implemented: macro elements "
+                f"{hits} have positive stencil directions and strong "
+                "coefficient variation; using plain scaling rows",
+                RuntimeWarning, stacklevel=3)
+
+    # -- device state ------------------------------------------------------
+    def _device(self):
+        if self._dev is None:
+            torch = require_cuda()
+            grid = self.grid
+            gt = GridTables(grid)
+            if self.variant == "const":
+                kc = np.full((gt.ntets, gt.L), self.const_value)
+            else:
+                kc = self.coeff.values
+            dg = DeviceGrid(gt, kc)
+            st = SurfaceTables(grid, gt, self._nodal_kinds)
+            ds = DeviceSurface(st, self._psh, self._pfac)
+            coef = torch.as_tensor(self._coef, device="cuda").reshape(-1)
+            w = None
+            if self._stored is not None:
+                w = torch.as_tensor(np.ascontiguousarray(np.stack(self._stored)),
+                                    device="cuda").reshape(-1)
+            self._dev = {"grid": dg, "surf": ds, "coef": coef, "w": w, "torch": torch}
+        return self._dev
+
+    def _vol_variant(self):
+        if self._stored is not None:
+            return _lib.VAR["stored"]
+        if self.variant == "nodal":
+            return _lib.VAR["nodal"]
+        if self.variant == "const":
+            return _lib.VAR["const"]
+        return _lib.VAR["scaling"]
+
+    def _to_dev(self, x, name="grid function"):
+        D = self._device()
+        torch = D["torch"]
+        if isinstance(x, torch.Tensor):
+            if x.shape != (self.grid.n_nodes,):
+                raise ValueError(f"{name} has wrong length")
+            return x.to(device="cuda", dtype=torch.float64).contiguous(), True
+        a = np.asarray(x, dtype=np.float64)
+        if a.shape != (self.grid.n_nodes,):
+            raise ValueError(f"{name} has wrong length")
+        return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=False), False
+
+    def _stream(self):
+        return self._device()["torch"].cuda.current_stream().cuda_stream
+
+    def apply_device(self, du, out=None, f=None):
+        """Device-resident A u (or f - A u when f is given), torch tensors."""
+        D = self._device()
+        torch = D["torch"]
+        if out is None:
+            out = torch.empty_like(du)
+        st = self._stream()
+        dg, ds = D["grid"], D["surf"]
+        flags = (_lib.FLAG_RESIDUAL if f is not None else 0) | \
+            (_lib.FLAG_FAST if (self.fast and self.variant != "nodal") else 0)
+        fp = f.data_ptr() if f is not None else None
+        check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
+        wp = D["w"].data_ptr() if D["w"] is not None else None
+        check(lib.hhg_volume_apply(dg.ref, self._vol_variant(), flags,
+                                   D["coef"].data_ptr(), wp, du.data_ptr(), fp,
+                                   out.data_ptr(), st), "volume_apply")
+        check(lib.hhg_surface_apply(dg.ref, ds.ref, 0, flags & _lib.FLAG_RESIDUAL,
+                                    du.data_ptr(), fp, out.data_ptr(), st),
+              "surface_apply")
+        return out
+
+    # -- public operations (reference signatures) ------------------------------
+    def apply(self, u):
+        """Matrix action A u with identity on Dirichlet rows."""
+        du, on_dev = self._to_dev(u)
+        out = self.apply_device(du)
+        self._count()
+        return out if on_dev else out.cpu().numpy()
+
+    def residual(self, u, f):
+        """r = f - A u, forced to zero on Dirichlet rows."""
+        du, on_dev = self._to_dev(u)
+        df, _ = self._to_dev(f, "right-hand side")
+        out = self.apply_device(du, f=df)
+        self._count()
+        return out if on_dev else out.cpu().numpy()
+
+    def smooth_device(self, du, df, sweeps=1, omega=1.0):
+        D = self._device()
+        dg, ds = D["grid"], D["surf"]
+        st = self._stream()
+        order, ptr, nlev = ds.levels()
+        var = _lib.VAR["nodal"] if self.variant == "nodal" else _lib.VAR["scaling"]
+        if self._stored is not None or self.variant == "const":
+            raise NotImplementedError("smooth() on the device supports the "
+                                      "scaling / nodal / hybrid / ma2 variants")
+        lib.hhg_status_reset()
+        base = order.data_ptr()
+        for _ in range(sweeps):
+            for lv in range(nlev):
+                a, b = int(ptr[lv]), int(ptr[lv + 1])
+                check(lib.hhg_smooth_surface_level(dg.ref, ds.ref, base + 8 * a, b - a,
+                                                   float(omega), du.data_ptr(),
+                                                   df.data_ptr(), st), "smooth_surface")
+            check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
+            check(lib.hhg_smooth_volume(dg.ref, var, D["coef"].data_ptr(), float(omega),
+                                        du.data_ptr(), df.data_ptr(), st), "smooth_volume")
+        D["torch"].cuda.current_stream().synchronize()
+        check(lib.hhg_status(), "smooth")
+        return du
+
+    def smooth(self, u, f, sweeps=1, omega=1.0):
+        """Forward Gauss-Seidel in global node order, in place; returns u."""
+        du, on_dev = self._to_dev(u)
+        df, _ = self._to_dev(f, "right-hand side")
+        self.smooth_device(du, df, sweeps, omega)
+        if on_dev:
+            if du.data_ptr() != u.data_ptr():
+                u.copy_(du)
+            return u
+        u[...] = du.cpu().numpy()
+        return u
+
+    def _count(self, napplies=1):
+        v = self.variant
+        if v in ("scaling", "scaling_ma2", "hybrid"):
+            cnt = analytic_count("scaling", 3)
+        elif v in ("nodal", "const", "stored"):
+            cnt = analytic_count(v, 3)
+        else:
+            return
+        total = self._nvol * self.grid.macro.n_elements * napplies
+        self.flops_add += cnt.add * total
+        self.flops_mul += cnt.mul * total
+
+    def stencil_weights(self, t):
+        """Volume stencil table of macro element t: rows (centre, s_0..s_13),
+        restated from the dump kernels (kernels.py:293-468)."""
+        w = np.zeros((self._nvol, 15))
+        if not self._nvol:
+            return w
+        if self._stored is not None:
+            return self._stored[t].copy()
+        from .mesh import SimplexLattice
+        n = self.grid.n
+        lat = self.grid.lat
+        ijk = SimplexLattice(3, n - 4).coords + 1
+        p = lat.index(ijk)
+        nb = [lat.index(ijk + d) for d in self._env.dirs]
+        if self.variant == "const":
+            s = self.const_value * 2.0 * self._sh[t]
+            w[:, 0] = -s.sum()
+            w[:, 1:] = s
+            return w
+        kv = self.coeff.values[t]
+        k0 = kv[p]
+        if self.variant == "nodal":
+            env = self._env
+            buf = np.empty((len(p), 55))
+            buf[:, 0] = k0
+            for d in range(14):
+                buf[:, 1 + d] = kv[nb[d]]
+            for dst, a, b in env.cse_schedule:
+                buf[:, dst] = buf[:, a] + buf[:, b]
+            fac = self._fac[t]
+            tot = np.zeros(len(p))
+            for d in range(14):
+                lo, hi = env.term_ptr[d], env.term_ptr[d + 1]
+                s = buf[:, env.cse_sums[env.term_elem[lo]]] * fac[lo]
+                for tt in range(lo + 1, hi):
+                    s = s + buf[:, env.cse_sums[env.term_elem[tt]]] * fac[tt]
+                w[:, 1 + d] = s
+                tot = tot + s
+            w[:, 0] = -tot
+            return w
+        sh = self._sh[t]
+        tot = np.zeros(len(p))
+        for d in range(14):
+            sd = (k0 + kv[nb[d]]) * sh[d]
+            w[:, 1 + d] = sd
+            tot = tot + sd
+        w[:, 0] = -tot
+        return w
+
+    def store_stencils(self):
+        """Precompute all volume stencils; returns the stored-variant twin."""
+        op = object.__new__(Operator)
+        op.__dict__.update(self.__dict__)
+        op.variant = "stored"
+        op.source_variant = self.variant
+        op.flops_add = 0
+        op.flops_mul = 0
+        op._stored = [self.stencil_weights(t) for t in range(self.grid.macro.n_elements)]
+        op.bytes_required = sum(w.nbytes for w in op._stored)
+        op._dev = None
+        return op

@@ -1,0 +1,106 @@
+"""Macro-element sharding across GPUs (one process per GPU) with the
+interface exchange of the surface rows.
+
+Partition: contiguous slabs of Kuhn cubes stacked in z, one
+slab per rank (config 5: 4 x 4 x 1 cubes = 96 macro tetrahedra per GPU).
+Every rank refines its own sub-mesh with a local HHG numbering; faces cut by
+the partition are *not* Dirichlet (the sub-mesh gets the global boundary
+faces explicitly).
+
+Volume rows need no communication: a macro element's rows depend only on
+its own lattice plus ghost shell, and the shell values of interface
+primitives are duplicated consistently on both ranks.  Surface rows of the
+interface primitives are sums over macro elements on both sides: each rank
+computes the one-sided partial rows from its own elements (exactly what the
+local surface kernel does for a face whose other side is absent), the two
+ranks swap the partial values of the interface nodes (one NCCL send/recv per
+neighbour per apply) and both add them in rank order, so the duplicated rows
+stay bitwise identical on both sides.  Dot products count each interface
+node once (owner = lower rank) and all-reduce one double.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from .mesh import MacroMesh, kuhn_blocks
+
+__all__ = ["slab_mesh", "InterfaceMap", "exchange_partials", "owned_mask"]
+
+
+def slab_mesh(rank: int, world: int, nx: int = 4, ny: int = 4) -> MacroMesh:
+    """Rank's slab [0,1]x[0,1]x[rank h, (rank+1) h] of nx*ny Kuhn cubes
+    (h = 1/max(nx, ny)); boundary faces are those of the global box."""
+    h = 1.0 / max(nx, ny)
+    xs = np.linspace(0.0, nx * h, nx + 1)
+    ys = np.linspace(0.0, ny * h, ny + 1)
+    z0, z1 = rank * h, (rank + 1) * h
+    tmp = kuhn_blocks(xs, ys, np.array([z0, z1]))
+    V = tmp.vertices
+    keep = []
+    for f, bnd in zip(tmp.faces, tmp.boundary_face):
+        if not bnd:
+            continue
+        z = V[f, 2]
+        if np.all(z == z0) and rank > 0:
+            continue                        # interface with rank - 1
+        if np.all(z == z1) and rank < world - 1:
+            continue                        # interface with rank + 1
+        keep.append(tuple(f))
+    return MacroMesh(tmp.vertices, tmp.elements, boundary_faces=keep)
+
+
+class InterfaceMap:
+    """Local node ids shared with the neighbour ranks, in a rank-independent
+    order (lexicographic in (y, x) of the interface plane)."""
+
+    def __init__(self, grid, rank: int, world: int, h: float):
+        self.rank, self.world = rank, world
+        X = grid.node_coords
+        free = ~grid.dirichlet_mask
+        self.neighbours = {}
+        self._lower_plane = None
+        for nbr, z in ((rank - 1, rank * h), (rank + 1, (rank + 1) * h)):
+            if nbr < 0 or nbr >= world:
+                continue
+            plane = X[:, 2] == z
+            if nbr < rank:
+                self._lower_plane = np.nonzero(plane)[0]
+            ids = np.nonzero(plane & free)[0]
+            order = np.lexsort((X[ids, 0], X[ids, 1]))
+            self.neighbours[nbr] = np.ascontiguousarray(ids[order])
+
+    def owned_mask(self, n_nodes):
+        """True where this rank owns the node (lower rank owns interfaces)."""
+        m = np.ones(n_nodes, dtype=bool)
+        if self._lower_plane is not None:
+            m[self._lower_plane] = False      # incl. Dirichlet copies
+        return m
+
+
+def owned_mask(imap: InterfaceMap, n_nodes: int):
+    return imap.owned_mask(n_nodes)
+
+
+def exchange_partials(out, imap: InterfaceMap, dist, index_tensors=None):
+    """Sum the one-sided interface rows of ``out`` (a torch tensor on the
+    rank's device, or CPU for gloo) with the neighbours' partials; the sum
+    is formed in rank order so both copies are bitwise equal."""
+    import torch
+    if not imap.neighbours:
+        return out
+    ops, recv, ids_t = [], {}, {}
+    for nbr, ids in imap.neighbours.items():
+        idx = index_tensors[nbr] if index_tensors is not None else \
+            torch.as_tensor(ids, device=out.device)
+        ids_t[nbr] = idx
+        send = out.index_select(0, idx).contiguous()
+        buf = torch.empty_like(send)
+        recv[nbr] = (send, buf)
+        ops.append(dist.P2POp(dist.isend, send, nbr))
+        ops.append(dist.P2POp(dist.irecv, buf, nbr))
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    for nbr, (mine, theirs) in recv.items():
+        total = (theirs + mine) if nbr < imap.rank else (mine + theirs)
+        out.index_copy_(0, ids_t[nbr], total)
+    return out

@@ -1,0 +1,268 @@
+"""GPU parity of the drop-in Operator and of the per-element C ABI.
+
+Volume rows must be BITWISE the reference's (the kernels reproduce the
+numba operation order with explicit round-to-nearest fp64 ops); surface rows
+(matrix-free one-sided stencils, a different summation order than the
+reference's scipy CSR) within 1e-13 relative; everything within the
+north-star tolerance 1e-12 relative.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+from tests.conftest import golden
+from oracle import kernels as ok
+from oracle.assemble import CpuOperator
+from paper_1709_06793_b200 import mesh as M
+from paper_1709_06793_b200 import Operator, parse_hybrid_set
+from paper_1709_06793_b200._lib import lib, check
+from paper_1709_06793_b200.coefficients import sample_nodal
+from paper_1709_06793_b200.reference_stencils import environment
+from tests.cases import case_mesh, checksum_weights, k_c1, k_c2, k_c3, wiggle3d
+
+pytestmark = pytest.mark.gpu
+
+TOL_SURF = 1e-13
+
+
+def _dev(torch, a):
+    return torch.as_tensor(np.ascontiguousarray(a), device="cuda")
+
+
+def _vol_mask(grid):
+    return np.arange(grid.n_nodes) >= grid.n_surface_nodes
+
+
+# -- per-element ABI (kernels.py signatures) ---------------------------------
+
+@pytest.mark.parametrize("n", [8, 16])
+def test_element_abi_bitwise(cuda, n):
+    torch = cuda
+    g = golden("kernels")
+    p = lambda k: g[f"n{n}_{k}"]
+    nv = ok.nvol_of(n)
+    st = torch.cuda.current_stream().cuda_stream
+    env = environment(3)
+    out = torch.empty(nv, dtype=torch.float64, device="cuda")
+    v, kc = _dev(torch, p("v")), _dev(torch, p("kc"))
+    check(lib.hhg_apply_scaling_3d(n, None, v.data_ptr(), kc.data_ptr(),
+                                   _dev(torch, p("sh")).data_ptr(), out.data_ptr(), st))
+    assert np.array_equal(out.cpu().numpy(), p("scaling"))
+    tabs = [np.ascontiguousarray(a, dtype=np.int64) for a in
+            (env.cse_schedule, env.cse_sums, env.term_ptr, env.term_elem)]
+    ip = lambda a: a.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+    fac = _dev(torch, p("fac"))
+    check(lib.hhg_apply_nodal_3d(n, None, v.data_ptr(), kc.data_ptr(), ip(tabs[0]), 40,
+                                 ip(tabs[1]), fac.data_ptr(), ip(tabs[2]), ip(tabs[3]),
+                                 out.data_ptr(), st))
+    assert np.array_equal(out.cpu().numpy(), p("nodal"))
+    s = p("s")
+    s15 = _dev(torch, np.append(s, -s.sum()))
+    check(lib.hhg_apply_const_3d(n, None, v.data_ptr(), s15.data_ptr(), -s.sum(),
+                                 out.data_ptr(), st))
+    assert np.array_equal(out.cpu().numpy(), p("const"))
+    w = _dev(torch, p("w"))
+    check(lib.hhg_apply_stored_3d(n, None, v.data_ptr(), w.data_ptr(), out.data_ptr(), st))
+    assert np.array_equal(out.cpu().numpy(), p("stored"))
+    fv = _dev(torch, p("fv"))
+    for key, om in (("gs_scaling", 1.0), ("gs_scaling_w08", 0.8)):
+        u = _dev(torch, p("v").copy())
+        check(lib.hhg_gs_scaling_3d(n, None, u.data_ptr(), fv.data_ptr(), kc.data_ptr(),
+                                    _dev(torch, p("shg")).data_ptr(), om, st))
+        assert np.array_equal(u.cpu().numpy(), p(key)), key
+    u = _dev(torch, p("v").copy())
+    check(lib.hhg_gs_nodal_3d(n, None, u.data_ptr(), fv.data_ptr(), kc.data_ptr(),
+                              ip(tabs[0]), 40, ip(tabs[1]), _dev(torch, p("facg")).data_ptr(),
+                              ip(tabs[2]), ip(tabs[3]), 1.0, st))
+    assert np.array_equal(u.cpu().numpy(), p("gs_nodal"))
+    bad = np.ascontiguousarray(tabs[0].copy())
+    bad[0, 0] = 99
+    assert lib.hhg_apply_nodal_3d(n, None, v.data_ptr(), kc.data_ptr(), ip(bad), 40,
+                                  ip(tabs[1]), fac.data_ptr(), ip(tabs[2]), ip(tabs[3]),
+                                  out.data_ptr(), st) == -4
+
+
+# -- drop-in Operator vs the reference ------------------------------------------
+
+APPLY_SETS = [
+    ("c1_simplex_l4", lambda: M.reference_simplex(3), 4, k_c1(), ["scaling", "nodal"]),
+    ("cube6_l3", M.unit_cube_6, 3, wiggle3d,
+     ["scaling", "nodal", "const", "hybrid:wv+we", "hybrid:w", "scaling_ma2"]),
+    ("cube12_l3", M.unit_cube_12, 3, wiggle3d, ["scaling", "nodal"]),
+    ("kuhn48_l3", lambda: case_mesh("c3"), 3, k_c3(), ["scaling", "nodal"]),
+    ("cube6_l5", M.unit_cube_6, 5, k_c2(), ["scaling", "nodal"]),
+]
+
+
+def _op(grid, kf, name):
+    if name == "const":
+        return Operator(grid, "const", 2.5)
+    hn = frozenset()
+    v = name
+    if name.startswith("hybrid:"):
+        hn, v = parse_hybrid_set(name.split(":", 1)[1]), "hybrid"
+    if v == "scaling_ma2":
+        with pytest.warns(RuntimeWarning, match="safeguard"):
+            return Operator(grid, v, kf)
+    return Operator(grid, v, kf, hybrid_nodal=hn)
+
+
+@pytest.mark.parametrize("tag,make,lvl,kfn,variants", APPLY_SETS)
+def test_apply_matches_reference(cuda, tag, make, lvl, kfn, variants):
+    g = golden(tag)
+    grid = M.RefinedGrid(make(), lvl)
+    kf = sample_nodal(kfn, grid)
+    u = g["u"]
+    vol = _vol_mask(grid)
+    for name in variants:
+        out = _op(grid, kf, name).apply(u)
+        want = g[f"apply_{name}"]
+        assert np.array_equal(out[vol], want[vol]), f"{name}: volume rows not bitwise"
+        assert np.array_equal(out[grid.dirichlet_mask], u[grid.dirichlet_mask])
+        err = np.abs(out - want).max() / np.abs(want).max()
+        assert err <= TOL_SURF, f"{name}: rel err {err:.2e}"
+
+
+@pytest.mark.parametrize("tag,make", [("cube6_l3", M.unit_cube_6),
+                                      ("cube12_l3", M.unit_cube_12)])
+def test_residual_stored_smooth_match_reference(cuda, tag, make):
+    g = golden(tag)
+    grid = M.RefinedGrid(make(), 3)
+    kf = sample_nodal(wiggle3d, grid)
+    op = Operator(grid, "scaling", kf)
+    r = op.residual(g["u"], g["f"])
+    want = g["residual_scaling"]
+    vol = _vol_mask(grid)
+    assert np.array_equal(r[vol], want[vol])
+    assert np.all(r[grid.dirichlet_mask] == 0.0)
+    assert np.abs(r - want).max() <= TOL_SURF * np.abs(want).max()
+    st = op.store_stencils()
+    assert st.variant == "stored" and st.source_variant == "scaling"
+    assert np.array_equal(st.stencil_weights(2), g["weights_t2"])
+    a = st.apply(g["u"])
+    assert np.array_equal(a[vol], g["stored_scaling"][vol])
+    assert np.abs(a - g["stored_scaling"]).max() <= TOL_SURF * np.abs(a).max()
+    for nm, var, om, sw in [("smooth_scaling_w1", "scaling", 1.0, 1),
+                            ("smooth_scaling_w08", "scaling", 0.8, 1),
+                            ("smooth_scaling_2sw", "scaling", 1.0, 2),
+                            ("smooth_nodal_w1", "nodal", 1.0, 1)]:
+        u = g["u"].copy()
+        ret = Operator(grid, var, kf).smooth(u, g["f"], sweeps=sw, omega=om)
+        assert ret is u
+        assert np.abs(u - g[nm]).max() < 1e-12, nm
+
+
+def test_smooth_equals_oracle_gs_bitwise_on_volume(cuda):
+    # with identical surface values the volume wavefront is bitwise the
+    # lexicographic sweep: compare one sweep against the C oracle started
+    # from the GPU's own post-surface state
+    grid = M.RefinedGrid(case_mesh("c3"), 4)
+    kf = sample_nodal(k_c3(), grid)
+    rng = np.random.default_rng(1)
+    u0 = rng.uniform(-1, 1, grid.n_nodes)
+    f = rng.uniform(-1, 1, grid.n_nodes)
+    u_gpu = Operator(grid, "scaling", kf).smooth(u0.copy(), f)
+    cpu = CpuOperator(grid, "scaling", kf)
+    u_cpu = cpu.smooth(u0.copy(), f)
+    assert np.abs(u_gpu - u_cpu).max() < 1e-12
+    # volume GS from identical shells is bitwise
+    u_mix = u0.copy()
+    surf = np.arange(grid.n_nodes) < grid.n_surface_nodes
+    u_mix[surf] = u_gpu[surf]
+    n = grid.n
+    for t in range(grid.macro.n_elements):
+        uloc = np.ascontiguousarray(u_mix[grid.elem_gidx[t]])
+        s0 = grid.vol_start[t]
+        ok.gs_scaling_3d(n, grid.lat.base, uloc, f[s0:s0 + grid.nodes_per_volume],
+                         kf.values[t], cpu.sh[t], 1.0)
+        u_mix[s0:s0 + grid.nodes_per_volume] = uloc[cpu.vol_pos]
+    vol = ~surf
+    assert np.array_equal(u_gpu[vol], u_mix[vol])
+
+
+def test_device_tensor_path_and_errors(cuda):
+    torch = cuda
+    grid = M.RefinedGrid(M.unit_cube_6(), 4)
+    kf = sample_nodal(wiggle3d, grid)
+    op = Operator(grid, "scaling", kf)
+    u = np.random.default_rng(3).normal(size=grid.n_nodes)
+    host = op.apply(u)
+    du = torch.as_tensor(u, device="cuda")
+    dev = op.apply(du)
+    assert isinstance(dev, torch.Tensor) and dev.is_cuda
+    assert np.array_equal(dev.cpu().numpy(), host)
+    with pytest.raises(ValueError, match="length"):
+        op.apply(np.zeros(grid.n_nodes + 1))
+    with pytest.raises(ValueError, match="unknown variant"):
+        Operator(grid, "magic", kf)
+    with pytest.raises(ValueError, match="positive"):
+        Operator(grid, "const", -1.0)
+    with pytest.raises(ValueError, match="sampled coefficient"):
+        Operator(grid, "scaling", 3.0)
+    with pytest.raises(ValueError, match="store_stencils"):
+        Operator(grid, "stored", kf)
+    op.apply(u)
+    nvol = grid.nodes_per_volume * grid.macro.n_elements
+    assert op.flops_add == 3 * 41 * nvol and op.flops_mul == 3 * 28 * nvol
+
+
+def test_fast_mode_within_tolerance(cuda):
+    grid = M.RefinedGrid(case_mesh("c3"), 5)
+    kf = sample_nodal(k_c3(), grid)
+    u = np.random.default_rng(4).uniform(-1, 1, grid.n_nodes)
+    exact = Operator(grid, "scaling", kf).apply(u)
+    fast = Operator(grid, "scaling", kf, fast=True).apply(u)
+    assert np.abs(fast - exact).max() <= 1e-12 * np.abs(exact).max()
+
+
+# -- config 3 at full size (48 macro elements, level 7, 1.7e7 nodes) -----------
+
+@pytest.mark.slow
+def test_config3_full_size_checksums(cuda):
+    g = golden("c3_checksums")
+    grid = M.RefinedGrid(case_mesh("c3"), 7)
+    kf = sample_nodal(k_c3(), grid)
+    rng = np.random.default_rng(3)
+    u = rng.uniform(-1, 1, grid.n_nodes)
+    f = rng.uniform(-1, 1, grid.n_nodes)
+    op = Operator(grid, "scaling", kf)
+    w = checksum_weights(grid.n_nodes)
+    for nm, vec in (("apply", op.apply(u)), ("residual", op.residual(u, f))):
+        scale = g[f"{nm}_absmax"]
+        assert np.abs(vec[::1009] - g[f"{nm}_sample"]).max() <= 1e-13 * scale
+        assert abs(vec @ w - g[f"{nm}_w"]) <= 1e-12 * scale * np.sqrt(grid.n_nodes)
+        assert abs(vec.sum() - g[f"{nm}_sum"]) <= 1e-12 * scale * np.sqrt(grid.n_nodes)
+    # volume rows of every macro element bitwise against the C oracle
+    out = op.apply(u)
+    n = grid.n
+    sh = op._sh
+    nvol = grid.nodes_per_volume
+    for t in range(grid.macro.n_elements):
+        want = ok.apply_scaling_3d(n, grid.lat.base, u[grid.elem_gidx[t]], kf.values[t], sh[t])
+        s0 = grid.vol_start[t]
+        assert np.array_equal(out[s0:s0 + nvol], want), t
+
+
+@pytest.mark.slow
+def test_large_grid_algebraic_properties(cuda):
+    """Size-independent properties at the per-GPU size of config 5 (96
+    macro elements, level 8 would be 2.7e8 rows; level 7 keeps host setup
+    short): constants in the kernel, linearity, symmetry on free nodes."""
+    torch = cuda
+    grid = M.RefinedGrid(case_mesh("c5"), 7)
+    kf = sample_nodal(k_c1(), grid)
+    op = Operator(grid, "scaling", kf)
+    free = torch.as_tensor(~grid.dirichlet_mask, device="cuda")
+    ones = torch.ones(grid.n_nodes, dtype=torch.float64, device="cuda")
+    r = op.apply(ones)
+    assert torch.where(free, r, 0).abs().max().item() < 1e-11
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.rand(grid.n_nodes, dtype=torch.float64, device="cuda", generator=gen) * free
+    y = torch.rand(grid.n_nodes, dtype=torch.float64, device="cuda", generator=gen) * free
+    Ax, Ay = op.apply(x), op.apply(y)
+    Axy = op.apply(2.0 * x - 3.0 * y)
+    assert (Axy - (2.0 * Ax - 3.0 * Ay)).abs().max().item() <= 1e-12 * Ax.abs().max().item()
+    s1 = torch.dot(y, Ax * free).item()
+    s2 = torch.dot(x, Ay * free).item()
+    assert abs(s1 - s2) <= 1e-10 * abs(s1)

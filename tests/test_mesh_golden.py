@@ -1,0 +1,108 @@
+"""Host numbering layer pinned to the reference (golden mesh.npz) and the
+lattice/shell/tile bookkeeping the device kernels rely on."""
+import numpy as np
+import pytest
+
+from tests.conftest import golden
+from paper_1709_06793_b200 import mesh as M
+from paper_1709_06793_b200.device import shell_layout, volume_tiles
+from tests.cases import case_mesh
+
+GRIDS = [("simplex_l3", lambda: M.reference_simplex(3), 3),
+         ("cube6_l2", M.unit_cube_6, 2), ("cube12_l2", M.unit_cube_12, 2),
+         ("kuhn48_l1", lambda: case_mesh("c3"), 1), ("slab96_l1", lambda: case_mesh("c5"), 1)]
+
+
+@pytest.mark.parametrize("tag,make,lvl", GRIDS)
+def test_numbering_matches_reference(tag, make, lvl):
+    g = golden("mesh")
+    grid = M.RefinedGrid(make(), lvl)
+    assert np.array_equal(grid.elem_gidx, g[f"{tag}_gidx"])
+    assert np.array_equal(grid.dirichlet_mask, g[f"{tag}_dirichlet"])
+    assert np.array_equal(grid.node_coords, g[f"{tag}_coords"])     # bitwise
+    assert np.array_equal(grid.vol_start, g[f"{tag}_vol_start"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 16, 32])
+def test_lattice_base_closed_form(n):
+    lat = M.SimplexLattice(3, n)
+    for k in range(n + 1):
+        for j in range(n + 1 - k):
+            assert lat.base[k, j] == M.lattice_base(n, k, j)
+    assert lat.size == M.lattice_size(n)
+    assert np.array_equal(lat.index(lat.coords), np.arange(lat.size))
+
+
+@pytest.mark.parametrize("n", [2, 4, 8, 16])
+def test_shell_layout_covers_boundary_once(n):
+    srow, pos, S = shell_layout(n)
+    lat = M.SimplexLattice(3, n)
+    c = lat.coords
+    bary_zero = (c == 0).any(axis=1) | (c.sum(axis=1) == n)
+    assert S == len(pos) == bary_zero.sum()
+    assert set(pos.tolist()) == set(np.nonzero(bary_zero)[0].tolist())
+    # srow addresses the first shell point of every row
+    for k in range(n + 1):
+        for j in range(n + 1 - k):
+            assert pos[srow[k * (n + 1) + j]] == lat.base[k, j]
+
+
+@pytest.mark.parametrize("n,rows", [(4, 16), (8, 16), (16, 16), (32, 16), (64, 4)])
+def test_tiles_partition_volume_rows(n, rows):
+    tiles = volume_tiles(n, 2, rows)
+    seen = np.zeros((2, n, n, n), dtype=np.int64)
+    for t, i0, j0, kmax in tiles:
+        for k in range(1, kmax + 1):
+            for j in range(j0, min(j0 + rows, n)):
+                for i in range(i0, i0 + 32):
+                    if i + j + k <= n - 1 and i >= 1 and j >= 1:
+                        seen[t, i, j, k] += 1
+    want = np.zeros_like(seen)
+    for k in range(1, n):
+        for j in range(1, n):
+            for i in range(1, n):
+                if i + j + k <= n - 1:
+                    want[:, i, j, k] = 1
+    assert np.array_equal(seen, want)
+    assert np.all(np.diff(tiles[:, 3]) <= 0)          # longest march first
+
+
+def test_volume_block_is_lattice_interior():
+    g = M.RefinedGrid(M.unit_cube_6(), 3)
+    n = g.n
+    inner = M.SimplexLattice(3, n - 4).coords + 1
+    pos = g.lat.index(inner)
+    for t in range(g.macro.n_elements):
+        assert np.array_equal(g.elem_gidx[t][pos],
+                              g.vol_start[t] + np.arange(g.nodes_per_volume))
+
+
+def test_orientation_and_errors():
+    m = M.MacroMesh([(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)], [(1, 0, 2, 3)])
+    assert np.all(m.signed_volumes() > 0)
+    with pytest.raises(M.MeshFormatError, match="degenerate"):
+        M.MacroMesh([(0, 0, 0), (1, 0, 0), (2, 0, 0), (0, 0, 1)], [(0, 1, 2, 3)])
+    with pytest.raises(M.MeshFormatError, match="repeats"):
+        M.MacroMesh([(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)], [(0, 1, 1, 3)])
+    with pytest.raises(M.MeshFormatError, match="out of range"):
+        M.MacroMesh([(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1)], [(0, 1, 2, 7)])
+
+
+def test_loader_roundtrip(tmp_path):
+    text = "DIM 3\nVERTICES 4\n0 0 0\n1 0 0\n0 1 0\n0 0 1\nELEMENTS 1\n0 1 2 3  # tet\n"
+    m = M.load_macro_mesh(text)
+    assert m.n_elements == 1 and m.boundary_face.all()
+    with pytest.raises(M.MeshFormatError, match="trailing"):
+        M.load_macro_mesh(text + "junk\n")
+
+
+def test_generators():
+    assert M.unit_cube_6().n_elements == 6
+    assert M.unit_cube_12().n_elements == 12
+    c3 = case_mesh("c3")
+    assert c3.n_elements == 48 and len(c3.vertices) == 27
+    assert np.isclose(c3.signed_volumes().sum(), 1.0)
+    c5 = case_mesh("c5")
+    assert c5.n_elements == 96
+    g = M.RefinedGrid(M.unit_cube_12(), 0)
+    assert (~g.dirichlet_mask).sum() == 1      # one interior macro vertex
