@@ -59,6 +59,11 @@ template <int SRC>
 static int dispatch_volume(const VolDesc &D, int variant, int flags, cudaStream_t st) {
   const bool res = flags & HHG_FLAG_RESIDUAL;
   const bool fast = flags & HHG_FLAG_FAST;
+#ifdef HHG_SCALING_ONLY  // tuning builds (tools/tune_volume.py)
+  if (variant != HHG_VAR_SCALING || res || SRC != SRC_SPLIT) return HHG_ERR_ARG;
+  return fast ? launch_volume<0, SRC, false, true>(D, st)
+              : launch_volume<0, SRC, false, false>(D, st);
+#endif
   switch (variant) {
     case HHG_VAR_SCALING:
       if (fast) return res ? launch_volume<0, SRC, true, true>(D, st)

@@ -17,6 +17,25 @@ __host__ __device__ __forceinline__ long long lbase(int n, int k, int j) {
          (long long)j * (j - 1) / 2;
 }
 
+// 32-bit forms for lattice-local offsets (exact for n <= 1000)
+__host__ __device__ __forceinline__ int tetra32(int m) {
+  return m < 0 ? 0 : (m + 1) * (m + 2) * (m + 3) / 6;
+}
+__host__ __device__ __forceinline__ int lbase32(int n, int k, int j) {
+  return tetra32(n) - tetra32(n - k) + j * (n + 1 - k) - j * (j - 1) / 2;
+}
+// offset of lattice row (k, j) inside the compact ghost shell of an element:
+// plane 0 is stored whole; plane k >= 1 stores its row j = 0, the two end
+// points of rows 1 .. n-k-1 and its last row (3 (n-k) points, 1 for k = n)
+__host__ __device__ __forceinline__ int srow32(int n, int k, int j) {
+  if (k == 0) return j * (n + 1) - j * (j - 1) / 2;
+  const int plane = (n + 1) * (n + 2) / 2 + 3 * ((k - 1) * n - (k - 1) * k / 2);
+  return plane + (j == 0 ? 0 : (n - k + 1) + 2 * (j - 1));
+}
+__host__ __device__ __forceinline__ long long shell_size(int n) {
+  return (long long)(n + 1) * (n + 2) / 2 + 3LL * n * (n - 1) / 2 + 1;
+}
+
 // the 14 stencil directions (di, dj, dk), mesh.py:44-48
 __constant__ int8_t c_dirs[14][3] = {
     {1, 0, 0},  {0, 1, 0},  {0, 0, 1},  {1, -1, 0},  {1, 0, -1},

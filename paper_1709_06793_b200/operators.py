@@ -163,7 +163,14 @@ class Operator:
             if self._stored is not None:
                 w = torch.as_tensor(np.ascontiguousarray(np.stack(self._stored)),
                                     device="cuda").reshape(-1)
-            self._dev = {"grid": dg, "surf": ds, "coef": coef, "w": w, "torch": torch}
+            sh = torch.as_tensor(np.ascontiguousarray(np.stack(self._sh)) if self._sh
+                                 else np.zeros((0, 14)), device="cuda").reshape(-1)
+            fac = None
+            if self._fac and self._fac[0] is not None:
+                fac = torch.as_tensor(np.ascontiguousarray(np.stack(self._fac)),
+                                      device="cuda").reshape(-1)
+            self._dev = {"grid": dg, "surf": ds, "coef": coef, "w": w, "torch": torch,
+                         "sh": sh, "fac": fac}
         return self._dev
 
     def _vol_variant(self):
@@ -176,16 +183,32 @@ class Operator:
         return _lib.VAR["scaling"]
 
     def _to_dev(self, x, name="grid function"):
+        """(device tensor, kind) with kind 'cuda' (device input, no copy),
+        'host' (CPU torch tensor: pinned-friendly non-blocking copy) or
+        'numpy' (reference contract: numpy in, numpy out)."""
         D = self._device()
         torch = D["torch"]
         if isinstance(x, torch.Tensor):
             if x.shape != (self.grid.n_nodes,):
                 raise ValueError(f"{name} has wrong length")
-            return x.to(device="cuda", dtype=torch.float64).contiguous(), True
+            if x.is_cuda:
+                return x.to(dtype=torch.float64).contiguous(), "cuda"
+            return x.to(device="cuda", dtype=torch.float64, non_blocking=True), "host"
         a = np.asarray(x, dtype=np.float64)
         if a.shape != (self.grid.n_nodes,):
             raise ValueError(f"{name} has wrong length")
-        return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=False), False
+        return torch.from_numpy(np.ascontiguousarray(a)).to("cuda"), "numpy"
+
+    def _from_dev(self, out, kind):
+        if kind == "cuda":
+            return out
+        torch = self._device()["torch"]
+        if kind == "host":
+            host = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+            host.copy_(out, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return host
+        return out.cpu().numpy()
 
     def _stream(self):
         return self._device()["torch"].cuda.current_stream().cuda_stream
@@ -209,33 +232,36 @@ class Operator:
         check(lib.hhg_surface_apply(dg.ref, ds.ref, 0, flags & _lib.FLAG_RESIDUAL,
                                     du.data_ptr(), fp, out.data_ptr(), st),
               "surface_apply")
+        self._count()
         return out
 
     # -- public operations (reference signatures) ------------------------------
     def apply(self, u):
         """Matrix action A u with identity on Dirichlet rows."""
-        du, on_dev = self._to_dev(u)
-        out = self.apply_device(du)
-        self._count()
-        return out if on_dev else out.cpu().numpy()
+        du, kind = self._to_dev(u)
+        return self._from_dev(self.apply_device(du), kind)
 
     def residual(self, u, f):
         """r = f - A u, forced to zero on Dirichlet rows."""
-        du, on_dev = self._to_dev(u)
+        du, kind = self._to_dev(u)
         df, _ = self._to_dev(f, "right-hand side")
-        out = self.apply_device(du, f=df)
-        self._count()
-        return out if on_dev else out.cpu().numpy()
+        return self._from_dev(self.apply_device(du, f=df), kind)
 
     def smooth_device(self, du, df, sweeps=1, omega=1.0):
+        """Forward GS on device tensors.  Surface rows level by level, ghost
+        refresh, then volume wavefronts.  const / stored smooth with the
+        scaling (or, for a nodal source, nodal) sweep: their stencil weights
+        are bitwise those rows ((c+c)*sh == (c*2)*sh; dumped weights are the
+        scaling/nodal row terms)."""
         D = self._device()
         dg, ds = D["grid"], D["surf"]
         st = self._stream()
         order, ptr, nlev = ds.levels()
-        var = _lib.VAR["nodal"] if self.variant == "nodal" else _lib.VAR["scaling"]
-        if self._stored is not None or self.variant == "const":
-            raise NotImplementedError("smooth() on the device supports the "
-                                      "scaling / nodal / hybrid / ma2 variants")
+        src = getattr(self, "source_variant", self.variant)
+        if src == "nodal":
+            var, coef = _lib.VAR["nodal"], D["coef"] if self._stored is None else D["fac"]
+        else:
+            var, coef = _lib.VAR["scaling"], D["sh"]
         lib.hhg_status_reset()
         base = order.data_ptr()
         for _ in range(sweeps):
@@ -245,7 +271,7 @@ class Operator:
                                                    float(omega), du.data_ptr(),
                                                    df.data_ptr(), st), "smooth_surface")
             check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
-            check(lib.hhg_smooth_volume(dg.ref, var, D["coef"].data_ptr(), float(omega),
+            check(lib.hhg_smooth_volume(dg.ref, var, coef.data_ptr(), float(omega),
                                         du.data_ptr(), df.data_ptr(), st), "smooth_volume")
         D["torch"].cuda.current_stream().synchronize()
         check(lib.hhg_status(), "smooth")
@@ -253,14 +279,13 @@ class Operator:
 
     def smooth(self, u, f, sweeps=1, omega=1.0):
         """Forward Gauss-Seidel in global node order, in place; returns u."""
-        du, on_dev = self._to_dev(u)
+        du, kind = self._to_dev(u)
         df, _ = self._to_dev(f, "right-hand side")
         self.smooth_device(du, df, sweeps, omega)
-        if on_dev:
-            if du.data_ptr() != u.data_ptr():
-                u.copy_(du)
-            return u
-        u[...] = du.cpu().numpy()
+        if kind == "numpy":
+            u[...] = du.cpu().numpy()
+        elif du.data_ptr() != u.data_ptr():
+            u.copy_(du)
         return u
 
     def _count(self, napplies=1):
