@@ -119,14 +119,26 @@ typedef struct hhg_surface {
   int64_t nrows;           /* non-Dirichlet surface rows                     */
   const int64_t *rows;     /* [nrows] global ids                             */
   const uint8_t *row_nodal;/* [nrows] 1: nodal-integration row (hybrid/nodal)*/
-  const int32_t *inc_ptr;  /* [nrows+1] incidences (macro element, point)    */
+  /* row-major incidences (macro element, boundary lattice point) per row,
+   * ordered by element: used by the Gauss-Seidel sweep                     */
+  const int32_t *inc_ptr;  /* [nrows+1]                                      */
   const int32_t *inc_tet;  /* [ninc]                                         */
-  const int32_t *inc_code; /* [ninc] i | j<<10 | k<<20 | class<<30? see .cu */
+  const int32_t *inc_code; /* [ninc] i | j << 10 | k << 20 (lattice coords)  */
   const uint8_t *inc_cls;  /* [ninc] boundary class 0..13                    */
   const double *psh;       /* [ntets*14*14] one-sided half stencils          */
   const double *pfac;      /* [ntets*14*72] one-sided nodal factors or NULL  */
   int64_t ndir;            /* Dirichlet rows                                 */
   const int64_t *dir_ids;  /* [ndir]                                         */
+  /* element-major copy of the incidences (lattice order inside each
+   * element) for the apply: partial rows are computed with coalesced
+   * lattice reads, then summed per row in element order                    */
+  int64_t ninc;
+  const int32_t *p_tet;    /* [ninc]                                         */
+  const int32_t *p_code;   /* [ninc]                                         */
+  const uint8_t *p_cls;    /* [ninc]                                         */
+  const uint8_t *p_nodal;  /* [ninc] row of this incidence is a nodal row    */
+  const int32_t *row_inc;  /* [ninc] element-major index, row-major order    */
+  double *partial;         /* [ninc] scratch                                 */
 } hhg_surface;
 
 /* refresh the ghost layers: ghost[e] = u[shell_gid[e]] */

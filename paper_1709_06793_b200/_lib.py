@@ -40,7 +40,9 @@ class HhgSurface(ctypes.Structure):
     _fields_ = [("nrows", ctypes.c_int64), ("rows", vp), ("row_nodal", vp),
                 ("inc_ptr", vp), ("inc_tet", vp), ("inc_code", vp),
                 ("inc_cls", vp), ("psh", vp), ("pfac", vp),
-                ("ndir", ctypes.c_int64), ("dir_ids", vp)]
+                ("ndir", ctypes.c_int64), ("dir_ids", vp),
+                ("ninc", ctypes.c_int64), ("p_tet", vp), ("p_code", vp),
+                ("p_cls", vp), ("p_nodal", vp), ("row_inc", vp), ("partial", vp)]
 
 
 # name -> (restype, argtypes); every symbol of include/hhg_b200.h

@@ -16,13 +16,17 @@
 using namespace hhg;
 
 #ifndef HHG_VOL_B
-#define HHG_VOL_B 2
+#define HHG_VOL_B 3
 #endif
 #ifndef HHG_VOL_W
-#define HHG_VOL_W 8
+#define HHG_VOL_W 4
 #endif
 #ifndef HHG_VOL_NS
-#define HHG_VOL_NS 6
+#define HHG_VOL_NS 8
+#endif
+
+#ifndef HHG_VOL_MINB
+#define HHG_VOL_MINB 2
 #endif
 
 static constexpr int kB = HHG_VOL_B, kW = HHG_VOL_W, kNS = HHG_VOL_NS;
@@ -40,18 +44,32 @@ static inline int check(const char *what) {
 // ---------------------------------------------------------------------------
 // volume kernel dispatch
 // ---------------------------------------------------------------------------
+// tile geometry: every variant covers kW*kB rows per tile (the host tile
+// list depends only on that product); the nodal kernel keeps one output row
+// per thread (its 55-slot element-sum buffer needs the registers)
+template <int VAR>
+struct VolGeom {
+  static constexpr int B = (VAR == 1) ? 1 : kB;
+  static constexpr int W = (VAR == 1) ? kW * kB : kW;
+};
+// tile = 32 columns x (W * B) rows; warps are 8 x 4 lane patches
+static_assert(kW % 4 == 0, "tile width is 4 warps of 8 columns");
+
 template <int VAR, int SRC, bool RES, bool FAST>
 static int launch_volume(const VolDesc &D, cudaStream_t st) {
   if (D.ntiles <= 0) return HHG_OK;
-  constexpr int ROWS = kW * kB + 2;
+  constexpr int B = VolGeom<VAR>::B, W = VolGeom<VAR>::W;
+  static_assert(B * W == kB * kW, "tile rows must not depend on the variant");
+  constexpr int ROWS = W * B + 2;
   const size_t smem = sizeof(double2) * kNS * ROWS * VOL_COLS + 72 * sizeof(double);
-  auto kern = volume_kernel<VAR, SRC, RES, FAST, kB, kW, kNS>;
+  constexpr int MINB = (VAR == 1) ? 1 : HHG_VOL_MINB;
+  auto kern = volume_kernel<VAR, SRC, RES, FAST, B, W, kNS, MINB>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  kern<<<D.ntiles, 32 * kW, smem, st>>>(D);
+  kern<<<D.ntiles, 32 * W, smem, st>>>(D);
   return check("volume_kernel");
 }
 
@@ -83,17 +101,15 @@ static int dispatch_volume(const VolDesc &D, int variant, int flags, cudaStream_
   return HHG_ERR_ARG;
 }
 
-// tiles of one macro element: 32 i-columns x (W*B) j-rows, k-march up to
-// kmax; longest first for load balance
+// tiles of the macro elements: 32 i-columns x (W*B) j-rows, k-march up to
+// kmax; (j-band, element, i) order as in device.volume_tiles
 static std::vector<int4> make_tiles(int n, int ntets) {
   std::vector<int4> tl;
   const int TJ = kW * kB;
-  for (int t = 0; t < ntets; ++t)
-    for (int j0 = 1; j0 <= n - 3; j0 += TJ)
+  for (int j0 = 1; j0 <= n - 3; j0 += TJ)
+    for (int t = 0; t < ntets; ++t)
       for (int i0 = 1; i0 + j0 <= n - 2; i0 += 32)
         tl.push_back(make_int4(t, i0, j0, n - 1 - i0 - j0));
-  std::stable_sort(tl.begin(), tl.end(),
-                   [](const int4 &a, const int4 &b) { return a.w > b.w; });
   return tl;
 }
 
@@ -292,6 +308,13 @@ static SurfDesc surf_desc(const hhg_grid *g, const hhg_surface *s) {
   D.inc_cls = s->inc_cls;
   D.psh = s->psh;
   D.pfac = s->pfac;
+  D.ninc = s->ninc;
+  D.p_tet = s->p_tet;
+  D.p_code = s->p_code;
+  D.p_cls = s->p_cls;
+  D.p_nodal = s->p_nodal;
+  D.row_inc = s->row_inc;
+  D.partial = s->partial;
   return D;
 }
 
@@ -303,10 +326,16 @@ int hhg_surface_apply(const hhg_grid *g, const hhg_surface *s, int, int flags,
   D.f = f;
   D.out = out;
   if (s->nrows > 0) {
-    const int blocks = (int)((s->nrows + 127) / 128);
-    if (res) surface_kernel<true><<<blocks, 128, 0, S(stream)>>>(D);
-    else surface_kernel<false><<<blocks, 128, 0, S(stream)>>>(D);
-    int rc = check("surface_kernel");
+    const bool mixed = s->pfac != nullptr;
+    const int pblocks = (int)((s->ninc + 127) / 128);
+    if (mixed) surface_partial_kernel<true><<<pblocks, 128, 0, S(stream)>>>(D);
+    else surface_partial_kernel<false><<<pblocks, 128, 0, S(stream)>>>(D);
+    int rc = check("surface_partial_kernel");
+    if (rc) return rc;
+    const int rblocks = (int)((s->nrows + 255) / 256);
+    if (res) surface_reduce_kernel<true><<<rblocks, 256, 0, S(stream)>>>(D);
+    else surface_reduce_kernel<false><<<rblocks, 256, 0, S(stream)>>>(D);
+    rc = check("surface_reduce_kernel");
     if (rc) return rc;
   }
   if (s->ndir > 0) {
@@ -373,7 +402,7 @@ int hhg_status_reset(void) {
   return HHG_OK;
 }
 
-int hhg_volume_tile_rows(void) { return kW * kB; }
+int hhg_volume_tile_rows(void) { return kW * kB; }   // W*B rows (W/4 warp rows of 4B)
 
 // host-side level schedule of the surface Gauss-Seidel: rows are in
 // ascending global id, dep_idx[dep_ptr[r]..dep_ptr[r+1]) lists the row
@@ -397,7 +426,8 @@ int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr, const int64_t *dep
 
 const char *hhg_build_info(void) {
   static char buf[128];
-  snprintf(buf, sizeof buf, "sm_100a volume B=%d W=%d NS=%d", kB, kW, kNS);
+  snprintf(buf, sizeof buf, "sm_100a volume B=%d W=%d NS=%d MINB=%d", kB, kW, kNS,
+           HHG_VOL_MINB);
   return buf;
 }
 

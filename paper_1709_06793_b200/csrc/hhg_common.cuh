@@ -42,6 +42,14 @@ __constant__ int8_t c_dirs[14][3] = {
     {0, 1, -1}, {1, -1, 1}, {-1, 0, 0}, {0, -1, 0},  {0, 0, -1},
     {-1, 1, 0}, {-1, 0, 1}, {0, -1, 1}, {-1, 1, -1}};
 
+// the same directions as compile-time constants (for unrolled loops)
+__host__ __device__ constexpr int c_dirs_h(int d, int c) {
+  constexpr int a[14][3] = {{1, 0, 0},  {0, 1, 0},  {0, 0, 1},  {1, -1, 0},  {1, 0, -1},
+                            {0, 1, -1}, {1, -1, 1}, {-1, 0, 0}, {0, -1, 0},  {0, 0, -1},
+                            {-1, 1, 0}, {-1, 0, 1}, {0, -1, 1}, {-1, 1, -1}};
+  return a[d][c];
+}
+
 // patch tables (reference_stencils.py:48-75 and Environment.term_*):
 // term t of direction d (t in [TPTR[d], TPTR[d+1])) reads element sum slot
 // 31 + TELEM[t].

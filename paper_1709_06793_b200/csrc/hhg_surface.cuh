@@ -26,28 +26,94 @@ struct SurfDesc {
   const int *inc_ptr, *inc_tet, *inc_code;
   const unsigned char *inc_cls;
   const double *psh, *pfac;
+  // element-major incidences
+  long long ninc;
+  const int *p_tet, *p_code;
+  const unsigned char *p_cls, *p_nodal;
+  const int *row_inc;
+  double *partial;
 };
 
-// value of lattice point (i, j, k) of element t from the global vector or the
-// element's ghost shell (same addressing as the volume staging)
-__device__ __forceinline__ double load_point(const SurfDesc &D, int t, int i,
-                                             int j, int k) {
-  const int n = D.n;
-  const int rowlen = n + 1 - k - j;
-  const bool inner = (k >= 1) && (j >= 1) && (k + j <= n - 2);
-  if (inner && i >= 1 && i <= rowlen - 2)
-    return D.u[D.vol_start[t] + lbase(n - 4, k - 1, j - 1) + i - 1];
-  const double *g = D.ghost + (long long)t * D.S + D.srow[k * (n + 1) + j];
-  return inner ? g[i == 0 ? 0 : 1] : g[i];
+// Lattice addressing of one incidence (point (i, j, k) of element t) and
+// its in-element neighbours, all in 32-bit closed forms.  Plane index
+// a = dk + 1 selects the precomputed constants of planes k-1, k, k+1.
+struct IncPlanes {
+  int kb[3], rk[3];   // lattice:  base(q, j) = kb + j*rk - j(j-1)/2
+  int ib[3], ri[3];   // inner lattice of the volume block (plane q-1)
+  int gb[3];          // shell offset of plane q (q >= 1)
+};
+
+__device__ __forceinline__ IncPlanes inc_planes(int n, int k) {
+  IncPlanes P;
+  const int m4 = n - 4;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int q = k - 1 + a;
+    P.kb[a] = tetra32(n) - tetra32(n - q);
+    P.rk[a] = n + 1 - q;
+    P.ib[a] = (q >= 1) ? tetra32(m4) - tetra32(m4 - (q - 1)) : 0;
+    P.ri[a] = n - 2 - q;
+    P.gb[a] = (q >= 1) ? (n + 1) * (n + 2) / 2 + 3 * ((q - 1) * n - (q - 1) * q / 2) : 0;
+  }
+  return P;
 }
 
-template <bool RES>
-__global__ void surface_kernel(SurfDesc D) {
+__device__ __forceinline__ int inc_koff(const IncPlanes &P, int a, int qi, int qj) {
+  return P.kb[a] + qj * P.rk[a] - qj * (qj - 1) / 2 + qi;
+}
+
+// offset of a lattice point's value: interior -> volume block (returns
+// true), shell -> compact ghost shell (returns false)
+__device__ __forceinline__ bool inc_voff(const IncPlanes &P, int a, int n, int qi, int qj,
+                                         int qk, int &off) {
+  const bool interior = qk >= 1 && qj >= 1 && qi >= 1 && qi + qj + qk <= n - 1;
+  if (interior) {
+    const int jj = qj - 1;
+    off = P.ib[a] + jj * P.ri[a] - jj * (jj - 1) / 2 + qi - 1;
+  } else if (qk == 0) {
+    off = qj * (n + 1) - qj * (qj - 1) / 2 + qi;
+  } else {
+    off = P.gb[a] + (qj == 0 ? qi : (n + 1 - qk) + 2 * (qj - 1) + (qi > 0 ? 1 : 0));
+  }
+  return interior;
+}
+
+// neighbour (v, k) pairs of one incidence for the apply; directions that
+// leave the macro element get (v0, 0) so they contribute exactly zero
+__device__ __forceinline__ void inc_gather(const SurfDesc &D, int t, int i, int j, int k,
+                                           unsigned mask, double v0, double2 (&q)[14],
+                                           double &k0) {
+  const int n = D.n;
+  const IncPlanes P = inc_planes(n, k);
+  const double *kt = D.kc + (long long)t * D.L;
+  const double *ut = D.u + D.vol_start[t];
+  const double *gt = D.ghost + (long long)t * D.S;
+  k0 = kt[inc_koff(P, 1, i, j)];
+#pragma unroll
+  for (int d = 0; d < 14; ++d) {
+    const int di = c_dirs_h(d, 0), dj = c_dirs_h(d, 1), dk = c_dirs_h(d, 2);
+    const int qi = i + di, qj = j + dj, qk = k + dk;
+    if (mask >> d & 1) {
+      int off;
+      const bool in = inc_voff(P, dk + 1, n, qi, qj, qk, off);
+      q[d].x = in ? ut[off] : gt[off];
+      q[d].y = kt[inc_koff(P, dk + 1, qi, qj)];
+    } else {
+      q[d].x = v0;
+      q[d].y = 0.0;
+    }
+  }
+}
+
+// MIXED = false: every row is a scaling row (no nodal factors on device)
+template <bool RES, bool MIXED>
+__global__ void __launch_bounds__(128)
+surface_kernel(SurfDesc D) {
   const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (r >= D.nrows) return;
   const long long gid = D.rows[r];
   const double v0 = D.u[gid];
-  const bool nodal = D.row_nodal[r] != 0;
+  const bool nodal = MIXED && D.row_nodal[r] != 0;
   double row = 0.0;
   for (int e = D.inc_ptr[r]; e < D.inc_ptr[r + 1]; ++e) {
     const int t = D.inc_tet[e];
@@ -55,34 +121,73 @@ __global__ void surface_kernel(SurfDesc D) {
     const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
     const int cls = D.inc_cls[e];
     const unsigned mask = c_cls_dirmask[cls];
-    const double *kt = D.kc + (long long)t * D.L;
-    const double k0 = kt[lbase(D.n, k, j) + i];
     double2 q[14];
-#pragma unroll
-    for (int d = 0; d < 14; ++d) {
-      if (mask >> d & 1) {
-        const int qi = i + c_dirs[d][0], qj = j + c_dirs[d][1], qk = k + c_dirs[d][2];
-        q[d].x = load_point(D, t, qi, qj, qk);
-        q[d].y = kt[lbase(D.n, qk, qj) + qi];
-      } else {  // outside the macro element: contributes exactly zero
-        q[d].x = v0;
-        q[d].y = 0.0;
-      }
-    }
+    double k0;
+    inc_gather(D, t, i, j, k, mask, v0, q, k0);
     double part;
-    if (!nodal) {
+    if (!MIXED || !nodal) {
       const double *sh = D.psh + ((long long)t * 14 + cls) * 14;
       part = 0.0;
 #pragma unroll
       for (int d = 0; d < 14; ++d)
         if (mask >> d & 1)
-          part = dadd(part, dmul(dmul(dadd(k0, q[d].y), sh[d]), dsub(q[d].x, v0)));
+          part = dadd(part, dmul(dmul(dadd(k0, q[d].y), __ldg(sh + d)), dsub(q[d].x, v0)));
     } else {
       const double *fac = D.pfac + ((long long)t * 14 + cls) * 72;
       part = nodal_row_exact(v0, k0, q, fac);
     }
     row = dadd(row, part);
   }
+  if (RES) row = dsub(D.f[gid], row);
+  D.out[gid] = row;
+}
+
+// pass 1: one thread per incidence in element-major (lattice) order — the
+// one-sided partial row of that boundary point; its own value comes from
+// the ghost shell, so neighbouring threads read neighbouring lattice points
+template <bool MIXED>
+__global__ void __launch_bounds__(128)
+surface_partial_kernel(SurfDesc D) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= D.ninc) return;
+  const int t = D.p_tet[e];
+  const int code = D.p_code[e];
+  const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+  const int cls = D.p_cls[e];
+  const unsigned mask = c_cls_dirmask[cls];
+  const int n = D.n;
+  const IncPlanes P = inc_planes(n, k);
+  int off;
+  inc_voff(P, 1, n, i, j, k, off);            // a boundary point: shell offset
+  const double v0 = D.ghost[(long long)t * D.S + off];
+  double2 q[14];
+  double k0;
+  inc_gather(D, t, i, j, k, mask, v0, q, k0);
+  double part;
+  if (!MIXED || !D.p_nodal[e]) {
+    const double *sh = D.psh + ((long long)t * 14 + cls) * 14;
+    part = 0.0;
+#pragma unroll
+    for (int d = 0; d < 14; ++d)
+      if (mask >> d & 1)
+        part = dadd(part, dmul(dmul(dadd(k0, q[d].y), __ldg(sh + d)), dsub(q[d].x, v0)));
+  } else {
+    const double *fac = D.pfac + ((long long)t * 14 + cls) * 72;
+    part = nodal_row_exact(v0, k0, q, fac);
+  }
+  D.partial[e] = part;
+}
+
+// pass 2: one thread per free surface row, partials summed in element
+// order (identical association to the one-pass kernel above)
+template <bool RES>
+__global__ void surface_reduce_kernel(SurfDesc D) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r >= D.nrows) return;
+  double row = 0.0;
+  for (int x = D.inc_ptr[r]; x < D.inc_ptr[r + 1]; ++x)
+    row = dadd(row, D.partial[D.row_inc[x]]);
+  const long long gid = D.rows[r];
   if (RES) row = dsub(D.f[gid], row);
   D.out[gid] = row;
 }

@@ -19,6 +19,12 @@ namespace hhg {
 
 constexpr int VOL_COLS = 34;  // 32 lanes + halo
 
+// ablation switch for tools/tune_volume.py (0 in every product build):
+// 1 = no arithmetic (store v0), 2 = no staging after the prologue
+#ifndef HHG_VOL_EXPT
+#define HHG_VOL_EXPT 0
+#endif
+
 struct VolDesc {
   int n, ntets;
   long long L, nvol, S;
@@ -48,6 +54,28 @@ __device__ __forceinline__ void cp_async_commit() {
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// mbarrier helpers (shared::cta)
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(unsigned bar) {
+  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(bar)
+               : "memory");
+}
+// arrive once all cp.async issued so far by this thread have landed
+__device__ __forceinline__ void mbar_arrive_cp_async(unsigned bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
 }
 
 // opaque copy: stops nvcc from re-folding the 64-bit element base
@@ -167,6 +195,67 @@ __device__ __forceinline__ void neighbours(const Win<B> &lo, const Win<B> &mi,
   q[13] = lo.L[s + 1];  // (-1, 1,-1)
 }
 
+// neighbour d of output row s (same mapping as neighbours())
+template <int B>
+__device__ __forceinline__ double2 nbr(const Win<B> &lo, const Win<B> &mi, const Win<B> &hi,
+                                       int d, int s) {
+  switch (d) {
+    case 0: return mi.R[s + 1];
+    case 1: return mi.C[s + 2];
+    case 2: return hi.C[s + 1];
+    case 3: return mi.R[s];
+    case 4: return lo.R[s + 1];
+    case 5: return lo.C[s + 2];
+    case 6: return hi.R[s];
+    case 7: return mi.L[s];
+    case 8: return mi.C[s];
+    case 9: return lo.C[s + 1];
+    case 10: return mi.L[s + 1];
+    case 11: return hi.L[s];
+    case 12: return hi.C[s];
+    default: return lo.L[s + 1];
+  }
+}
+
+// all B scaling rows of a thread, direction-outer / row-inner so the B
+// accumulation chains interleave (warps issue in order: independent chains
+// placed side by side hide the FP64 latency).  Per row the association is
+// exactly the reference's: acc = ((t0 + t1) + t2) + ... with
+// t_d = ((k0 + kq) * sh[d]) * (vq - v0).
+template <int B, bool FAST>
+__device__ __forceinline__ void scaling_rows(const Win<B> &lo, const Win<B> &mi,
+                                             const Win<B> &hi, const double (&sh)[14],
+                                             double (&out)[B]) {
+  double v0[B], k0[B];
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    v0[s] = mi.C[s + 1].x;
+    k0[s] = mi.C[s + 1].y;
+  }
+  if (!FAST) {
+#pragma unroll
+    for (int d = 0; d < 14; ++d)
+#pragma unroll
+      for (int s = 0; s < B; ++s) {
+        const double2 q = nbr<B>(lo, mi, hi, d, s);
+        const double term = dmul(dmul(dadd(k0[s], q.y), sh[d]), dsub(q.x, v0[s]));
+        out[s] = (d == 0) ? term : dadd(out[s], term);
+      }
+  } else {
+#pragma unroll
+    for (int s = 0; s < B; ++s) out[s] = 0.0;
+#pragma unroll
+    for (int d = 0; d < 7; ++d)
+#pragma unroll
+      for (int s = 0; s < B; ++s) {
+        const double2 a = nbr<B>(lo, mi, hi, d, s), b = nbr<B>(lo, mi, hi, d + 7, s);
+        double m = (k0[s] + a.y) * (a.x - v0[s]);
+        m = fma(k0[s] + b.y, b.x - v0[s], m);
+        out[s] = fma(sh[d], m, out[s]);
+      }
+  }
+}
+
 template <int VAR, bool FAST>
 struct RowOp;
 
@@ -229,10 +318,10 @@ struct RowOp<3, FAST> {  // stored stencils w[c] = (diag, s_0..s_13)
   }
 };
 
-template <int VAR, int SRC, bool RES, bool FAST, int B, int W, int NS>
-__global__ void __launch_bounds__(32 * W, 1)
+template <int VAR, int SRC, bool RES, bool FAST, int B, int W, int NS, int MINB>
+__global__ void __launch_bounds__(32 * W, MINB)
 volume_kernel(VolDesc D) {
-  constexpr int ROWS = W * B + 2;
+  constexpr int ROWS = W * B + 2;          // (W/4 warps) x (4 lane rows) x B
   constexpr int NT = 32 * W;
   constexpr int NSLOT = (ROWS * VOL_COLS + NT - 1) / NT;
   constexpr unsigned PLANE_BYTES = ROWS * VOL_COLS * sizeof(double2);
@@ -282,24 +371,52 @@ volume_kernel(VolDesc D) {
     S.dst = ring_s + (unsigned)e * sizeof(double2);
   }
 
-  auto stage = [&](int p) {
+  // ring of NS plane slots with a full / empty mbarrier pair each: a slot
+  // is "full" when every thread's cp.async for it has landed (NT async
+  // arrivals) and "empty" when every warp has copied its window out of it
+  // (W arrivals).  Warps drift freely up to the prefetch distance PD
+  // instead of meeting at a CTA barrier every plane.
+  constexpr int PD = NS - 2;
+  __shared__ __align__(8) unsigned long long bars[2 * NS];
+  const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(&bars[0]));
+  const unsigned empty0 = full0 + NS * 8;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(full0 + 8 * b, NT);
+      mbar_init(empty0 + 8 * b, W);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  auto produce = [&](int p) {
+    const int sl = p % NS;
+    if (p >= NS) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
     const PlaneConst P = plane_const(n, p);
-    const unsigned off = (unsigned)(p % NS) * PLANE_BYTES;
+    const unsigned off = (unsigned)sl * PLANE_BYTES;
+    if (HHG_VOL_EXPT != 2 || p < PD) {
 #pragma unroll
-    for (int m = 0; m < NSLOT; ++m) stage_slot<SRC>(T, slots[m], P, n, p, off);
+      for (int m = 0; m < NSLOT; ++m) stage_slot<SRC>(T, slots[m], P, n, p, off);
+    }
+    mbar_arrive_cp_async(full0 + 8 * sl);
   };
 
-  // prologue: planes 0 .. NS-2 in flight
-#pragma unroll
-  for (int p = 0; p < NS - 1; ++p) {
-    if (p <= kmax + 1) stage(p);
-    cp_async_commit();
-  }
+  // prologue: planes 0 .. PD-1 in flight
+  for (int p = 0; p < PD && p <= kmax + 1; ++p) produce(p);
 
-  const int r0 = 1 + warp * B;  // first tile row of this thread
-  const int c = 1 + lane;
-  const int i = i0 + lane;
-  const int jw = j0 + warp * B;
+  // lane layout: a warp is an 8 (i) x 4 (row groups) patch, warps side by
+  // side in i, each thread B consecutive rows of one column.  A warp's
+  // lanes then span only 8 + 4B - 1 diagonal levels i + j, so few lanes sit
+  // past the element's slanted face, and a warp whose lowest i + j is
+  // already invalid skips the arithmetic altogether.
+  static_assert(W % 4 == 0, "4 warps of 8 lanes cover the 32 tile columns");
+  const int li = lane & 7, lj = lane >> 3;
+  const int wi = warp & 3, wj = warp >> 2;   // warps: 4 along i, W/4 along j
+  const int r0 = 1 + wj * 4 * B + lj * B;  // first tile row of this thread
+  const int c = 1 + wi * 8 + li;
+  const int i = i0 + wi * 8 + li;
+  const int jw = j0 + wj * 4 * B + lj * B;
+  const int warp_min_ij = i0 + wi * 8 + j0 + wj * 4 * B;
   const int m4 = n - 4;
   // per output row s: -(jj)(jj-1)/2 + i - 1 with jj = j - 1
   int oterm[B];
@@ -312,36 +429,49 @@ volume_kernel(VolDesc D) {
   Win<B> X0, X1, X2;
 
   auto step = [&](int q, Win<B> &lo, Win<B> &mi, Win<B> &hi) {
-    // plane q has landed for this thread; make everyone's copies visible
-    cp_async_wait<NS - 2>();
-    __syncthreads();
-    const int pf = q + NS - 1;
-    if (pf <= kmax + 1) stage(pf);
-    cp_async_commit();
-    load_win<B>(hi, ring + (q % NS) * ROWS * VOL_COLS, r0, c);
-    if (q >= 2) {
+    const int sl = q % NS;
+    mbar_wait(full0 + 8 * sl, (q / NS) & 1);
+    load_win<B>(hi, ring + sl * ROWS * VOL_COLS, r0, c);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * sl);
+    if (q >= 2 && warp_min_ij <= n - q) {   // some lane of the warp is valid
       const int kk = q - 1;
       const int lim = n - 1 - kk;  // valid outputs: i + j <= lim
       // volume rank of (i, j, kk): inner-lattice row (kk-1, j-1) + i - 1
       const int iplane = tetra32(m4) - tetra32(m4 - (kk - 1));
       const int rowi = m4 + 2 - kk;
+      double vals[B];
+      if constexpr (VAR == 0 && HHG_VOL_EXPT == 1) {
+#pragma unroll
+        for (int s = 0; s < B; ++s) vals[s] = mi.C[s + 1].x + lo.R[s + 1].y + hi.L[s].x;
+      } else if constexpr (VAR == 0) {
+        scaling_rows<B, FAST>(lo, mi, hi, op.sh, vals);
+      } else {
+#pragma unroll
+        for (int s = 0; s < B; ++s) {
+          double2 nb[14];
+          neighbours<B>(lo, mi, hi, s, nb);
+          const double2 ctr = mi.C[s + 1];
+          const int cidx = iplane + (jw + s - 1) * rowi + oterm[s];
+          const bool valid = i + jw + s <= lim;
+          vals[s] = 0.0;
+          if (VAR != 3 || valid) vals[s] = op(ctr.x, ctr.y, nb, cidx);  // stored reads w[cidx]
+        }
+      }
 #pragma unroll
       for (int s = 0; s < B; ++s) {
-        double2 nb[14];
-        neighbours<B>(lo, mi, hi, s, nb);
-        const double2 ctr = mi.C[s + 1];
-        const int cidx = iplane + (jw + s - 1) * rowi + oterm[s];
-        // invalid lanes compute on stale shared data; only the store is
+        // invalid lanes computed on stale shared data; only the store is
         // predicated (no divergent branch around the arithmetic)
-        const bool valid = i + jw + s <= lim;
-        double val = 0.0;
-        if (VAR != 3 || valid) val = op(ctr.x, ctr.y, nb, cidx);  // stored reads w[cidx]
-        if (valid) {
+        if (i + jw + s <= lim) {
+          const int cidx = iplane + (jw + s - 1) * rowi + oterm[s];
+          double val = vals[s];
           if (RES) val = dsub(__ldg(at(T.f, cidx)), val);
-          *at(T.o, cidx) = val;
+          __stcs(at(T.o, cidx), val);
         }
       }
     }
+    const int pf = q + PD;
+    if (pf <= kmax + 1) produce(pf);
   };
 
   for (int q = 0; q <= kmax + 1; q += 3) {

@@ -64,19 +64,24 @@ def shell_layout(n: int):
     return srow, pos, off
 
 
-def volume_tiles(n: int, ntets: int, tile_rows: int):
-    """(tet, i0, j0, kmax) work tiles, longest k-march first (stable)."""
+TILE_GROUP = 8   # macro elements whose j-bands are interleaved (L2 reuse)
+
+
+def volume_tiles(n: int, ntets: int, tile_rows: int, group: int = TILE_GROUP):
+    """(tet, i0, j0, kmax) work tiles ordered by (element group, j-band,
+    element, i): tiles sharing a halo column run back to back, and a band's
+    halo rows are re-read by the next band of the same element while they
+    are still in L2 (a group of 8 level-8 elements streams ~50 MB between
+    the two reads); deep k-marches (low j-bands) start first in each group."""
     tl = []
-    for j0 in range(1, n - 2, tile_rows):
-        for i0 in range(1, n - 1 - j0, 32):
-            tl.append((i0, j0, n - 1 - i0 - j0))
-    if not tl or ntets == 0:
+    for g0 in range(0, ntets, group):
+        for j0 in range(1, n - 2, tile_rows):
+            for t in range(g0, min(g0 + group, ntets)):
+                for i0 in range(1, n - 1 - j0, 32):
+                    tl.append((t, i0, j0, n - 1 - i0 - j0))
+    if not tl:
         return np.zeros((0, 4), dtype=np.int32)
-    base = np.array(tl, dtype=np.int32)
-    t = np.repeat(np.arange(ntets, dtype=np.int32), len(base))
-    allt = np.column_stack([t, np.tile(base, (ntets, 1))])
-    order = np.argsort(-allt[:, 3], kind="stable")
-    return np.ascontiguousarray(allt[order])
+    return np.ascontiguousarray(np.array(tl, dtype=np.int32))
 
 
 class GridTables:
@@ -139,6 +144,18 @@ class SurfaceTables:
         kinds = grid.node_kind[self.rows]
         self.row_nodal = np.isin(kinds, [int(k) for k in nodal_kinds]).astype(np.uint8)
         self.dir_ids = np.nonzero(grid.dirichlet_mask)[0].astype(np.int64)
+        # element-major copy: incidence order (tet, shell position) = lattice
+        # order inside each element; row_inc maps row-major -> element-major
+        key = self.inc_tet.astype(np.int64) * gt.S + spos
+        emaj = np.argsort(key, kind="stable")
+        self.p_tet = np.ascontiguousarray(self.inc_tet[emaj])
+        self.p_code = np.ascontiguousarray(self.inc_code[emaj])
+        self.p_cls = np.ascontiguousarray(self.inc_cls[emaj])
+        row_of_inc = np.repeat(np.arange(len(self.rows)), np.diff(self.inc_ptr))
+        self.p_nodal = np.ascontiguousarray(self.row_nodal[row_of_inc][emaj])
+        inv = np.empty_like(emaj)
+        inv[emaj] = np.arange(len(emaj))
+        self.row_inc = np.ascontiguousarray(inv.astype(np.int32))
         self._grid = grid
         self._gt = gt
 
@@ -236,6 +253,12 @@ class DeviceSurface:
         self.psh = t(psh)
         self.pfac = t(pfac) if pfac is not None else None
         self.dir_ids = t(st.dir_ids)
+        self.p_tet = t(st.p_tet)
+        self.p_code = t(st.p_code)
+        self.p_cls = t(st.p_cls)
+        self.p_nodal = t(st.p_nodal)
+        self.row_inc = t(st.row_inc)
+        self.partial = torch.empty(max(len(st.p_tet), 1), dtype=torch.float64, device=dev)
         d = HhgSurface()
         d.nrows = len(st.rows)
         d.rows = self.rows.data_ptr()
@@ -248,6 +271,13 @@ class DeviceSurface:
         d.pfac = self.pfac.data_ptr() if self.pfac is not None else None
         d.ndir = len(st.dir_ids)
         d.dir_ids = self.dir_ids.data_ptr()
+        d.ninc = len(st.p_tet)
+        d.p_tet = self.p_tet.data_ptr()
+        d.p_code = self.p_code.data_ptr()
+        d.p_cls = self.p_cls.data_ptr()
+        d.p_nodal = self.p_nodal.data_ptr()
+        d.row_inc = self.row_inc.data_ptr()
+        d.partial = self.partial.data_ptr()
         self.desc = d
         self.ref = ctypes.byref(d)
         self._levels = None

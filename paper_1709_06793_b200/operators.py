@@ -182,7 +182,7 @@ class Operator:
             return _lib.VAR["const"]
         return _lib.VAR["scaling"]
 
-    def _to_dev(self, x, name="grid function"):
+    def _to_dev(self, x, name="grid function", pipelined=False):
         """(device tensor, kind) with kind 'cuda' (device input, no copy),
         'host' (CPU torch tensor: pinned-friendly non-blocking copy) or
         'numpy' (reference contract: numpy in, numpy out)."""
@@ -193,6 +193,8 @@ class Operator:
                 raise ValueError(f"{name} has wrong length")
             if x.is_cuda:
                 return x.to(dtype=torch.float64).contiguous(), "cuda"
+            if pipelined and x.dtype == torch.float64 and x.is_contiguous():
+                return x, "host-pipe"
             return x.to(device="cuda", dtype=torch.float64, non_blocking=True), "host"
         a = np.asarray(x, dtype=np.float64)
         if a.shape != (self.grid.n_nodes,):
@@ -235,10 +237,105 @@ class Operator:
         self._count()
         return out
 
+    # -- host-buffer pipeline ---------------------------------------------------
+    def _pipeline(self, groups=8):
+        """Streams, events and per-group tile descriptors of apply_host."""
+        if getattr(self, "_pipe", None) is None:
+            import ctypes
+            D = self._device()
+            torch = D["torch"]
+            grid, dg = self.grid, D["grid"]
+            ne = grid.macro.n_elements
+            ng = max(1, min(groups, ne))
+            bounds = np.linspace(0, ne, ng + 1).astype(int)
+            tiles = dg.gt.tiles
+            descs, keep = [], []
+            for g in range(ng):
+                sel = (tiles[:, 0] >= bounds[g]) & (tiles[:, 0] < bounds[g + 1])
+                tg = torch.as_tensor(np.ascontiguousarray(tiles[sel]), device="cuda")
+                d = type(dg.desc).from_buffer_copy(dg.desc)
+                d.tiles = tg.data_ptr() if len(tg) else None
+                d.ntiles = int(sel.sum())
+                descs.append(d)
+                keep.append(tg)
+            n = grid.n_nodes
+            self._pipe = {
+                "bounds": bounds, "descs": descs, "keep": keep,
+                "streams": [torch.cuda.Stream() for _ in range(3)],
+                "du": torch.empty(n, dtype=torch.float64, device="cuda"),
+                "out": torch.empty(n, dtype=torch.float64, device="cuda"),
+                "host_out": torch.empty(n, dtype=torch.float64, pin_memory=True),
+                "byref": ctypes.byref,
+            }
+        return self._pipe
+
+    def apply_host(self, u_host):
+        """A u for a (pinned) CPU tensor, H2D / kernels / D2H overlapped per
+        group of macro elements: the surface block goes first (the ghost
+        update needs only surface values), each group's volume block is
+        applied as soon as it has landed and copied back while the next
+        group is in flight; the surface rows (which read interior values of
+        every element) run last.  Returns a pinned CPU tensor."""
+        D = self._device()
+        torch = D["torch"]
+        P = self._pipeline()
+        grid, dg, ds = self.grid, D["grid"], D["surf"]
+        h2d, comp, d2h = P["streams"]
+        du, out, hout = P["du"], P["out"], P["host_out"]
+        ns = grid.n_surface_nodes
+        vs = grid.vol_start
+        nv = grid.nodes_per_volume
+        flags = _lib.FLAG_FAST if (self.fast and self.variant != "nodal") else 0
+        wp = D["w"].data_ptr() if D["w"] is not None else None
+        cur = torch.cuda.current_stream()
+        for st in P["streams"]:
+            st.wait_stream(cur)
+        ev_in = []
+        with torch.cuda.stream(h2d):
+            du[:ns].copy_(u_host[:ns], non_blocking=True)
+            e = torch.cuda.Event()
+            e.record(h2d)
+            ev_in.append(e)
+            for g in range(len(P["descs"])):
+                a, b = int(vs[P["bounds"][g]]) if nv else ns, \
+                    int(vs[P["bounds"][g + 1] - 1] + nv) if nv else ns
+                if b > a:
+                    du[a:b].copy_(u_host[a:b], non_blocking=True)
+                e = torch.cuda.Event()
+                e.record(h2d)
+                ev_in.append(e)
+        comp.wait_event(ev_in[0])
+        cs = comp.cuda_stream
+        check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), cs), "ghost_update")
+        for g, desc in enumerate(P["descs"]):
+            comp.wait_event(ev_in[g + 1])
+            check(lib.hhg_volume_apply(P["byref"](desc), self._vol_variant(), flags,
+                                       D["coef"].data_ptr(), wp, du.data_ptr(), None,
+                                       out.data_ptr(), cs), "volume_apply")
+            e = torch.cuda.Event()
+            e.record(comp)
+            d2h.wait_event(e)
+            if nv:
+                a, b = int(vs[P["bounds"][g]]), int(vs[P["bounds"][g + 1] - 1] + nv)
+                with torch.cuda.stream(d2h):
+                    hout[a:b].copy_(out[a:b], non_blocking=True)
+        check(lib.hhg_surface_apply(dg.ref, ds.ref, 0, 0, du.data_ptr(), None,
+                                    out.data_ptr(), cs), "surface_apply")
+        e = torch.cuda.Event()
+        e.record(comp)
+        d2h.wait_event(e)
+        with torch.cuda.stream(d2h):
+            hout[:ns].copy_(out[:ns], non_blocking=True)
+        d2h.synchronize()
+        self._count()
+        return hout
+
     # -- public operations (reference signatures) ------------------------------
     def apply(self, u):
         """Matrix action A u with identity on Dirichlet rows."""
-        du, kind = self._to_dev(u)
+        du, kind = self._to_dev(u, pipelined=True)
+        if kind == "host-pipe":
+            return self.apply_host(du)
         return self._from_dev(self.apply_device(du), kind)
 
     def residual(self, u, f):

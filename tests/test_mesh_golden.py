@@ -64,7 +64,8 @@ def test_tiles_partition_volume_rows(n, rows):
                 if i + j + k <= n - 1:
                     want[:, i, j, k] = 1
     assert np.array_equal(seen, want)
-    assert np.all(np.diff(tiles[:, 3]) <= 0)          # longest march first
+    for t in range(2):                                 # deep j-bands first
+        assert np.all(np.diff(tiles[tiles[:, 0] == t, 2]) >= 0)
 
 
 def test_volume_block_is_lattice_interior():
