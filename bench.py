@@ -160,7 +160,7 @@ def run_own(args):
         st = torch.cuda.current_stream()
         s = st.cuda_stream
         dg, ds = D["grid"], D["surf"]
-        flags = _lib.FLAG_FAST if (op.fast and op.variant != "nodal") else 0
+        flags = op._vol_flags()
         check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), s))
         if record:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -253,7 +253,9 @@ def run_own(args):
                                    f"level {args.level}", "level": args.level,
                        "macro_tets_per_gpu": ntets, "dofs_per_gpu": int(grid.n_nodes),
                        "volume_dofs_per_gpu": int(nvol_rank), "variant": args.variant,
-                       "arithmetic": "fast-fma" if args.fast else "bitwise-reference-order",
+                       "arithmetic": "fast-fma" if args.fast else
+                       ("bitwise-reference-order, mirror edge reuse" if op._mirror
+                        else "bitwise-reference-order"),
                        "parallelism": f"macro-tet slabs x{world}",
                        "l2": "inputs larger than L2 (2.2 GB per vector)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,

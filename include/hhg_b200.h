@@ -44,6 +44,9 @@ extern "C" {
 /* flags */
 #define HHG_FLAG_RESIDUAL 1 /* write f - A u instead of A u               */
 #define HHG_FLAG_FAST 2     /* FMA / mirror-pair reassociated arithmetic   */
+#define HHG_FLAG_MIRROR 4   /* caller guarantees sh[d] == sh[d+7] bitwise
+                               for every element: edge terms shared by two
+                               rows are evaluated once (result unchanged)  */
 
 /* ---------------------------------------------------------------------
  * (1) per-macro-element kernels (lattice layout of one element)

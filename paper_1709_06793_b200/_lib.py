@@ -11,13 +11,13 @@ import os
 from pathlib import Path
 
 __all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "check", "HhgError",
-           "VAR", "FLAG_RESIDUAL", "FLAG_FAST", "EXPORTS"]
+           "VAR", "FLAG_RESIDUAL", "FLAG_FAST", "FLAG_MIRROR", "EXPORTS"]
 
 LIB_PATH = Path(__file__).resolve().parent / "libhhg_b200.so"
 
 HHG_OK, HHG_ERR_ARG, HHG_ERR_CUDA, HHG_ERR_ZERO_DIAG, HHG_ERR_TABLE = 0, -1, -2, -3, -4
 VAR = {"scaling": 0, "nodal": 1, "const": 2, "stored": 3}
-FLAG_RESIDUAL, FLAG_FAST = 1, 2
+FLAG_RESIDUAL, FLAG_FAST, FLAG_MIRROR = 1, 2, 4
 
 c_i64p = ctypes.POINTER(ctypes.c_int64)
 vp = ctypes.c_void_p

@@ -55,7 +55,7 @@ struct VolGeom {
 // tile = 32 columns x (W * B) rows; warps are 8 x 4 lane patches
 static_assert(kW % 4 == 0, "tile width is 4 warps of 8 columns");
 
-template <int VAR, int SRC, bool RES, bool FAST>
+template <int VAR, int SRC, bool RES, bool FAST, bool MIRROR = false>
 static int launch_volume(const VolDesc &D, cudaStream_t st) {
   if (D.ntiles <= 0) return HHG_OK;
   constexpr int B = VolGeom<VAR>::B, W = VolGeom<VAR>::W;
@@ -63,7 +63,7 @@ static int launch_volume(const VolDesc &D, cudaStream_t st) {
   constexpr int ROWS = W * B + 2;
   const size_t smem = sizeof(double2) * kNS * ROWS * VOL_COLS + 72 * sizeof(double);
   constexpr int MINB = (VAR == 1) ? 1 : HHG_VOL_MINB;
-  auto kern = volume_kernel<VAR, SRC, RES, FAST, B, W, kNS, MINB>;
+  auto kern = volume_kernel<VAR, SRC, RES, FAST, B, W, kNS, MINB, MIRROR>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -73,19 +73,43 @@ static int launch_volume(const VolDesc &D, cudaStream_t st) {
   return check("volume_kernel");
 }
 
+#ifndef HHG_MIRROR_MINB
+#define HHG_MIRROR_MINB 2
+#endif
+
+template <int SRC, bool RES>
+static int launch_mirror(const VolDesc &D, cudaStream_t st) {
+  if (D.ntiles <= 0) return HHG_OK;
+  static_assert(kW == 4, "the mirror kernel uses 4 warps of 8x4 lanes");
+  constexpr int ROWS = kW * kB + 2;
+  const size_t smem = sizeof(double2) * kNS * ROWS * VOL_COLS;
+  auto kern = volume_kernel_mirror<SRC, RES, kB, kNS, HHG_MIRROR_MINB>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = true;
+  }
+  kern<<<D.ntiles, 128, smem, st>>>(D);
+  return check("volume_kernel_mirror");
+}
+
 template <int SRC>
 static int dispatch_volume(const VolDesc &D, int variant, int flags, cudaStream_t st) {
   const bool res = flags & HHG_FLAG_RESIDUAL;
   const bool fast = flags & HHG_FLAG_FAST;
+  const bool mirror = flags & HHG_FLAG_MIRROR;
 #ifdef HHG_SCALING_ONLY  // tuning builds (tools/tune_volume.py)
   if (variant != HHG_VAR_SCALING || res || SRC != SRC_SPLIT) return HHG_ERR_ARG;
-  return fast ? launch_volume<0, SRC, false, true>(D, st)
-              : launch_volume<0, SRC, false, false>(D, st);
+  if (fast) return launch_volume<0, SRC, false, true>(D, st);
+  return mirror ? launch_mirror<SRC, false>(D, st)
+                : launch_volume<0, SRC, false, false>(D, st);
 #endif
   switch (variant) {
     case HHG_VAR_SCALING:
       if (fast) return res ? launch_volume<0, SRC, true, true>(D, st)
                            : launch_volume<0, SRC, false, true>(D, st);
+      if (mirror) return res ? launch_mirror<SRC, true>(D, st)
+                             : launch_mirror<SRC, false>(D, st);
       return res ? launch_volume<0, SRC, true, false>(D, st)
                  : launch_volume<0, SRC, false, false>(D, st);
     case HHG_VAR_NODAL:

@@ -256,6 +256,67 @@ __device__ __forceinline__ void scaling_rows(const Win<B> &lo, const Win<B> &mi,
   }
 }
 
+// Mirror-exact variant.  When sh[d] == sh[d+7] bitwise (checked on the
+// host), the reference term of an edge seen from its other end is the exact
+// negation:  ((k_q + k_p) * sh) * (v_p - v_q) == -(((k_p + k_q) * sh) *
+// (v_q - v_p))  in IEEE arithmetic, and  acc + (-t) == acc - t.  Edges whose
+// both ends belong to the same thread are therefore evaluated once:
+//   (0,-1, 0) of row s      = -(0,1,0) of row s-1      (same plane)
+//   (0, 0,-1) of plane kk   = -(0,0,1) of plane kk-1   (previous step)
+//   (0, 1,-1) of row s      = -(0,-1,1) of row s+1, plane kk-1
+// 3B-2 of the 14B terms per step are reused; the result is bitwise the
+// reference's.  pt2 / pt12 carry the (0,0,1) / (0,-1,1) terms to the next
+// step; `first` seeds them from plane kk-1 at the start of a tile.
+template <int B>
+__device__ __forceinline__ double edge_term(double2 p, double2 q, double sh) {
+  return dmul(dmul(dadd(p.y, q.y), sh), dsub(q.x, p.x));
+}
+
+template <int B>
+__device__ __forceinline__ void scaling_rows_mirror(const Win<B> &lo, const Win<B> &mi,
+                                                    const Win<B> &hi, const double (&sh)[14],
+                                                    double (&pt2)[B], double (&pt12)[B],
+                                                    bool first, double (&out)[B]) {
+  if (first) {  // (0,0,1) and (0,-1,1) terms of the points of plane kk-1
+#pragma unroll
+    for (int s = 0; s < B; ++s) {
+      pt2[s] = edge_term<B>(lo.C[s + 1], mi.C[s + 1], sh[2]);
+      pt12[s] = edge_term<B>(lo.C[s + 1], mi.C[s], sh[12]);
+    }
+  }
+  double t1[B], t2[B], t12[B];
+#pragma unroll
+  for (int d = 0; d < 14; ++d)
+#pragma unroll
+    for (int s = 0; s < B; ++s) {
+      const double2 c = mi.C[s + 1];
+      double t;
+      bool neg = false;
+      if (d == 8 && s >= 1) {
+        t = t1[s - 1];
+        neg = true;
+      } else if (d == 9) {
+        t = pt2[s];
+        neg = true;
+      } else if (d == 5 && s + 1 < B) {
+        t = pt12[s + 1];
+        neg = true;
+      } else {
+        t = edge_term<B>(c, nbr<B>(lo, mi, hi, d, s), sh[d]);
+        if (d == 1) t1[s] = t;
+        if (d == 2) t2[s] = t;
+        if (d == 12) t12[s] = t;
+      }
+      if (d == 0) out[s] = t;
+      else out[s] = neg ? dsub(out[s], t) : dadd(out[s], t);
+    }
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    pt2[s] = t2[s];
+    pt12[s] = t12[s];
+  }
+}
+
 template <int VAR, bool FAST>
 struct RowOp;
 
@@ -318,7 +379,8 @@ struct RowOp<3, FAST> {  // stored stencils w[c] = (diag, s_0..s_13)
   }
 };
 
-template <int VAR, int SRC, bool RES, bool FAST, int B, int W, int NS, int MINB>
+template <int VAR, int SRC, bool RES, bool FAST, int B, int W, int NS, int MINB,
+          bool MIRROR = false>
 __global__ void __launch_bounds__(32 * W, MINB)
 volume_kernel(VolDesc D) {
   constexpr int ROWS = W * B + 2;          // (W/4 warps) x (4 lane rows) x B
@@ -427,6 +489,7 @@ volume_kernel(VolDesc D) {
   }
 
   Win<B> X0, X1, X2;
+  double pt2[B], pt12[B];   // mirror-reuse carry (MIRROR only)
 
   auto step = [&](int q, Win<B> &lo, Win<B> &mi, Win<B> &hi) {
     const int sl = q % NS;
@@ -444,6 +507,8 @@ volume_kernel(VolDesc D) {
       if constexpr (VAR == 0 && HHG_VOL_EXPT == 1) {
 #pragma unroll
         for (int s = 0; s < B; ++s) vals[s] = mi.C[s + 1].x + lo.R[s + 1].y + hi.L[s].x;
+      } else if constexpr (VAR == 0 && MIRROR && !FAST) {
+        scaling_rows_mirror<B>(lo, mi, hi, op.sh, pt2, pt12, q == 2, vals);
       } else if constexpr (VAR == 0) {
         scaling_rows<B, FAST>(lo, mi, hi, op.sh, vals);
       } else {
@@ -480,6 +545,215 @@ volume_kernel(VolDesc D) {
     step(q + 1, X2, X0, X1);
     if (q + 2 > kmax + 1) break;
     step(q + 2, X0, X1, X2);
+  }
+  cp_async_wait<0>();
+}
+
+// ---------------------------------------------------------------------------
+// Default scaling kernel (bitwise reference order, mirror edge reuse) on a
+// register diet: the terms of output plane kk+1 that involve plane kk-... are
+// produced one step early, so only two planes of the window are live during
+// the arithmetic; only sh[0..6] are held; staging slots keep one packed
+// register.  Same tiles, ring, mbarriers and lane layout as volume_kernel.
+// ---------------------------------------------------------------------------
+template <int B>
+struct MirrorCarry {
+  double t2[B];    // (0,0,1) term of each row at plane kk   -> (0,0,-1) at kk+1
+  double t12[B];   // (0,-1,1) term of each row at plane kk  -> (0,1,-1) at kk+1
+  double t4[B];    // (1,0,-1) term of each row at plane kk+1 (neighbour on kk)
+  double t13[B];   // (-1,1,-1) term of each row at plane kk+1
+  double t5;       // (0,1,-1) term of the last row at plane kk+1
+};
+
+template <int B>
+__device__ __forceinline__ void mirror_seed(const Win<B> &lo, const Win<B> &mi,
+                                           const double (&sh)[7], MirrorCarry<B> &c) {
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    c.t2[s] = edge_term<B>(lo.C[s + 1], mi.C[s + 1], sh[2]);
+    c.t12[s] = edge_term<B>(lo.C[s + 1], mi.C[s], sh[5]);      // sh[12] == sh[5]
+    c.t4[s] = edge_term<B>(mi.C[s + 1], lo.R[s + 1], sh[4]);
+    c.t13[s] = edge_term<B>(mi.C[s + 1], lo.L[s + 1], sh[6]);  // sh[13] == sh[6]
+  }
+  c.t5 = edge_term<B>(mi.C[B], lo.C[B + 1], sh[5]);
+}
+
+// rows of plane kk from windows mi (kk) and hi (kk+1) plus the carry;
+// leaves the carry for plane kk+1.  Accumulation order d = 0..13 exactly.
+template <int B>
+__device__ __forceinline__ void mirror_step(const Win<B> &mi, const Win<B> &hi,
+                                            const double (&sh)[7], MirrorCarry<B> &c,
+                                            double (&out)[B]) {
+  double t1[B], n2[B], n12[B];
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const double2 p = mi.C[s + 1];
+    double a = edge_term<B>(p, mi.R[s + 1], sh[0]);                 // d 0
+    const double t1s = edge_term<B>(p, mi.C[s + 2], sh[1]);         // d 1
+    t1[s] = t1s;
+    a = dadd(a, t1s);
+    n2[s] = edge_term<B>(p, hi.C[s + 1], sh[2]);                    // d 2
+    a = dadd(a, n2[s]);
+    a = dadd(a, edge_term<B>(p, mi.R[s], sh[3]));                   // d 3
+    a = dadd(a, c.t4[s]);                                           // d 4
+    a = (s + 1 < B) ? dsub(a, c.t12[s + 1]) : dadd(a, c.t5);        // d 5
+    a = dadd(a, edge_term<B>(p, hi.R[s], sh[6]));                   // d 6
+    a = dadd(a, edge_term<B>(p, mi.L[s], sh[0]));                   // d 7
+    a = (s >= 1) ? dsub(a, t1[s - 1]) : dadd(a, edge_term<B>(p, mi.C[s], sh[1]));  // d 8
+    a = dsub(a, c.t2[s]);                                           // d 9
+    a = dadd(a, edge_term<B>(p, mi.L[s + 1], sh[3]));               // d 10
+    a = dadd(a, edge_term<B>(p, hi.L[s], sh[4]));                   // d 11
+    n12[s] = edge_term<B>(p, hi.C[s], sh[5]);                       // d 12
+    a = dadd(a, n12[s]);
+    a = dadd(a, c.t13[s]);                                          // d 13
+    out[s] = a;
+  }
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    c.t2[s] = n2[s];
+    c.t12[s] = n12[s];
+    c.t4[s] = edge_term<B>(hi.C[s + 1], mi.R[s + 1], sh[4]);
+    c.t13[s] = edge_term<B>(hi.C[s + 1], mi.L[s + 1], sh[6]);
+  }
+  c.t5 = edge_term<B>(hi.C[B], mi.C[B + 1], sh[5]);
+}
+
+template <int SRC, bool RES, int B, int NS, int MINB>
+__global__ void __launch_bounds__(128, MINB)
+volume_kernel_mirror(VolDesc D) {
+  constexpr int W = 4;
+  constexpr int ROWS = W * B + 2;
+  constexpr int NT = 32 * W;
+  constexpr int NSLOT = (ROWS * VOL_COLS + NT - 1) / NT;
+  constexpr unsigned PLANE_BYTES = ROWS * VOL_COLS * sizeof(double2);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2 *ring = reinterpret_cast<double2 *>(smem_raw);
+  const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(ring));
+
+  const int4 tile = D.tiles[blockIdx.x];
+  const int t = tile.x, i0 = tile.y, j0 = tile.z, kmax = tile.w;
+  const int n = D.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  TileBase T;
+  T.k = opaque(D.kc + (long long)t * D.L);
+  if (SRC == SRC_SPLIT) {
+    const long long vs = D.vol_start[t];
+    T.v = opaque(D.u + vs);
+    T.g = opaque(D.ghost + (long long)t * D.S);
+    T.o = opaque(D.out + vs);
+    T.f = RES ? opaque(D.f + vs) : nullptr;
+  } else {
+    T.v = opaque(D.u + (long long)t * D.L);
+    T.g = nullptr;
+    T.o = opaque(D.out + (long long)t * D.nvol);
+    T.f = RES ? opaque(D.f + (long long)t * D.nvol) : nullptr;
+  }
+  double sh[7];
+#pragma unroll
+  for (int d = 0; d < 7; ++d) sh[d] = __ldg(D.coef + (long long)t * D.coef_stride + d);
+
+  constexpr int PD = NS - 2;
+  __shared__ __align__(8) unsigned long long bars[2 * NS];
+  const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(&bars[0]));
+  const unsigned empty0 = full0 + NS * 8;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(full0 + 8 * b, NT);
+      mbar_init(empty0 + 8 * b, W);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  auto produce = [&](int p) {
+    const int sl = p % NS;
+    if (p >= NS) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
+    const PlaneConst P = plane_const(n, p);
+    const unsigned off = (unsigned)sl * PLANE_BYTES;
+#pragma unroll
+    for (int m = 0; m < NSLOT; ++m) {
+      const int e = threadIdx.x + m * NT;
+      if (e < ROWS * VOL_COLS) {
+        Slot S;
+        const int r = e / VOL_COLS, cc = e - r * VOL_COLS;
+        S.live = true;
+        S.i = i0 - 1 + cc;
+        S.j = j0 - 1 + r;
+        S.jk = -S.j * (S.j - 1) / 2 + S.i;
+        S.ji = -(S.j - 1) * (S.j - 2) / 2 + S.i - 1;
+        S.g0 = S.j * (n + 1) - S.j * (S.j - 1) / 2 + S.i;
+        S.gin = (S.j == 0) ? S.i : (n + 1) + 2 * (S.j - 1) + (S.i == 0 ? 0 : 1);
+        S.dst = ring_s + (unsigned)e * sizeof(double2);
+        stage_slot<SRC>(T, S, P, n, p, off);
+      }
+    }
+    mbar_arrive_cp_async(full0 + 8 * sl);
+  };
+
+  for (int p = 0; p < PD && p <= kmax + 1; ++p) produce(p);
+
+  const int li = lane & 7, lj = lane >> 3;
+  const int r0 = 1 + lj * B;
+  const int c = 1 + warp * 8 + li;
+  const int i = i0 + warp * 8 + li;
+  const int jw = j0 + lj * B;
+  const int warp_min_ij = i0 + warp * 8 + j0;
+  const int m4 = n - 4;
+  int oterm[B];
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const int jj = jw + s - 1;
+    oterm[s] = -jj * (jj - 1) / 2 + i - 1;
+  }
+
+  Win<B> X0, X1, X2;
+  MirrorCarry<B> carry;
+
+  // fetch plane q into window w and release its slot
+  auto fetch = [&](int q, Win<B> &w) {
+    const int sl = q % NS;
+    mbar_wait(full0 + 8 * sl, (q / NS) & 1);
+    load_win<B>(w, ring + sl * ROWS * VOL_COLS, r0, c);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * sl);
+    if (q + PD <= kmax + 1) produce(q + PD);
+  };
+  auto emit = [&](int kk, const double (&vals)[B]) {
+    const int lim = n - 1 - kk;
+    const int iplane = tetra32(m4) - tetra32(m4 - (kk - 1));
+    const int rowi = m4 + 2 - kk;
+#pragma unroll
+    for (int s = 0; s < B; ++s)
+      if (i + jw + s <= lim) {
+        const int cidx = iplane + (jw + s - 1) * rowi + oterm[s];
+        double val = vals[s];
+        if (RES) val = dsub(__ldg(at(T.f, cidx)), val);
+        __stcs(at(T.o, cidx), val);
+      }
+  };
+  // output plane kk = q - 1 from mi (plane kk) and hi (plane kk + 1)
+  auto step = [&](int q, Win<B> &mi, Win<B> &hi) {
+    fetch(q, hi);
+    if (warp_min_ij <= n - q) {   // some lane of the warp is valid
+      double vals[B];
+      mirror_step<B>(mi, hi, sh, carry, vals);
+      emit(q - 1, vals);
+    }
+  };
+
+  if (kmax >= 1) {
+    fetch(0, X0);
+    fetch(1, X1);
+    if (warp_min_ij <= n - 2) mirror_seed<B>(X0, X1, sh, carry);
+    step(2, X1, X2);
+    for (int q = 3; q <= kmax + 1; q += 3) {
+      step(q, X2, X0);
+      if (q + 1 > kmax + 1) break;
+      step(q + 1, X0, X1);
+      if (q + 2 > kmax + 1) break;
+      step(q + 2, X1, X2);
+    }
   }
   cp_async_wait<0>();
 }

@@ -37,7 +37,7 @@ for B, W, NS, MINB, EXPT in configs:
     so = f"/tmp/hhg_tune_{B}_{W}_{NS}_{MINB}_{EXPT}.so"
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-DHHG_SCALING_ONLY",
-           f"-DHHG_VOL_B={B}", f"-DHHG_VOL_W={W}", f"-DHHG_VOL_NS={NS}", f"-DHHG_VOL_MINB={MINB}", f"-DHHG_VOL_EXPT={EXPT}", "-Xptxas", "-v",
+           f"-DHHG_VOL_B={B}", f"-DHHG_VOL_W={W}", f"-DHHG_VOL_NS={NS}", f"-DHHG_VOL_MINB={MINB}", f"-DHHG_MIRROR_MINB={MINB}", f"-DHHG_VOL_EXPT={EXPT}", "-Xptxas", "-v",
            "-o", so, str(ROOT / "paper_1709_06793_b200/csrc/hhg_b200.cu")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
@@ -52,7 +52,7 @@ for B, W, NS, MINB, EXPT in configs:
     dg = DeviceGrid(gt, kf.values)
     st = torch.cuda.current_stream().cuda_stream
     h.hhg_ghost_update(dg.ref, u.data_ptr(), st)
-    for fast in (0, 2):
+    for fast in (0, 2, 4):
         for _ in range(3):
             h.hhg_volume_apply(dg.ref, 0, fast, sh.data_ptr(), None, u.data_ptr(), None, out.data_ptr(), st)
         torch.cuda.synchronize()
@@ -64,6 +64,6 @@ for B, W, NS, MINB, EXPT in configs:
         ms = e0.elapsed_time(e1) / 20
         chk = float(out[grid.n_surface_nodes:].abs().sum())
         if ref is None and EXPT == 0: ref = chk
-        print(f"B={B} W={W} NS={NS} MINB={MINB} EXPT={EXPT} fast={fast//2} {ms:.3f} ms {nvol/ms/1e6:.1f} GDoF/s "
+        print(f"B={B} W={W} NS={NS} MINB={MINB} EXPT={EXPT} flags={fast} {ms:.3f} ms {nvol/ms/1e6:.1f} GDoF/s "
               f"regs={regs[0].split('Used')[1].split(',')[0].strip() if regs else '?'} chk_ok={ref is not None and abs(chk-ref)<=1e-9*ref}", flush=True)
     del dg
