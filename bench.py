@@ -170,8 +170,7 @@ def run_own(args):
         if record:
             e1.record(st)
             vol_ev.append((e0, e1))
-        check(lib.hhg_surface_apply(dg.ref, ds.ref, 0, 0, du.data_ptr(), None,
-                                    out.data_ptr(), s))
+        op._surface(dg, ds, 0, du, None, out, s)
         if imap is not None:
             exchange_partials(out, imap, dist, idx_t)
 

@@ -193,6 +193,31 @@ int hhg_smooth_surface_level(const hhg_grid *g, const hhg_surface *s,
                              const int64_t *level_rows, int64_t count,
                              double omega, double *u, const double *f,
                              void *stream);
+/* precomputed surface rows of the smoother (level schedule + each row's
+ * neighbour ids and weights in accumulation order); all DEVICE arrays */
+typedef struct hhg_surface_gs {
+  const int64_t *level_rows;  /* [nrows] rows ordered by level               */
+  const int64_t *level_ptr;   /* [nlev+1]                                     */
+  int64_t nlev;
+  const int64_t *ent_ptr;     /* [nrows+1]                                    */
+  int32_t *ent_col;           /* [nent] global ids (filled by _prepare)       */
+  double *ent_val;            /* [nent] weights (filled by _prepare)          */
+  double *row_diag;           /* [nrows] diagonals (filled by _prepare)       */
+} hhg_surface_gs;
+
+/* apply / residual of the surface rows (+ Dirichlet rows) from the rows
+ * precomputed by hhg_smooth_surface_prepare; bitwise the matrix-free
+ * surface kernels' result (the weights are the factors they recompute) */
+int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s,
+                          const hhg_surface_gs *gs, int flags, const double *u,
+                          const double *f, double *out, void *stream);
+
+int hhg_smooth_surface_prepare(const hhg_grid *g, const hhg_surface *s,
+                               const hhg_surface_gs *gs, void *stream);
+/* every level of the surface sweep in one cooperative launch */
+int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s,
+                           const hhg_surface_gs *gs, double omega, double *u,
+                           const double *f, void *stream);
 int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef,
                       double omega, double *u, const double *f, void *stream);
 

@@ -10,7 +10,7 @@ import ctypes
 import os
 from pathlib import Path
 
-__all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "check", "HhgError",
+__all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "HhgSurfaceGS", "check", "HhgError",
            "VAR", "FLAG_RESIDUAL", "FLAG_FAST", "FLAG_MIRROR", "EXPORTS"]
 
 LIB_PATH = Path(__file__).resolve().parent / "libhhg_b200.so"
@@ -45,6 +45,11 @@ class HhgSurface(ctypes.Structure):
                 ("p_cls", vp), ("p_nodal", vp), ("row_inc", vp), ("partial", vp)]
 
 
+class HhgSurfaceGS(ctypes.Structure):
+    _fields_ = [("level_rows", vp), ("level_ptr", vp), ("nlev", ctypes.c_int64),
+                ("ent_ptr", vp), ("ent_col", vp), ("ent_val", vp), ("row_diag", vp)]
+
+
 # name -> (restype, argtypes); every symbol of include/hhg_b200.h
 EXPORTS = {
     "hhg_apply_scaling_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp]),
@@ -69,6 +74,17 @@ EXPORTS = {
                                                 ctypes.POINTER(HhgSurface), vp,
                                                 ctypes.c_int64, ctypes.c_double,
                                                 vp, vp, vp]),
+    "hhg_smooth_surface_prepare": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                                  ctypes.POINTER(HhgSurface),
+                                                  ctypes.POINTER(HhgSurfaceGS), vp]),
+    "hhg_surface_apply_csr": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                             ctypes.POINTER(HhgSurface),
+                                             ctypes.POINTER(HhgSurfaceGS), ctypes.c_int,
+                                             vp, vp, vp, vp]),
+    "hhg_smooth_surface_all": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                              ctypes.POINTER(HhgSurface),
+                                              ctypes.POINTER(HhgSurfaceGS), ctypes.c_double,
+                                              vp, vp, vp]),
     "hhg_smooth_volume": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int, vp,
                                          ctypes.c_double, vp, vp, vp]),
     "hhg_dot": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),

@@ -238,6 +238,41 @@ int hhg_apply_stored_3d(int64_t n, const int64_t *, const double *v, const doubl
   return dispatch_volume<SRC_LATTICE>(D, HHG_VAR_STORED, 0, S(stream));
 }
 
+// interior points of each hyperplane h = i + 2j + 3k (host-built once per n)
+struct Hyperplanes {
+  int n = -1;
+  int *ptr = nullptr, *code = nullptr;
+};
+static Hyperplanes g_hp;
+
+static int hyperplanes(int n, const int **ptr, const int **code) {
+  if (g_hp.n != n) {
+    const int hmin = 6, hmax = 3 * n - 6;
+    std::vector<int> p(hmax - hmin + 2, 0), c;
+    for (int h = hmin; h <= hmax; ++h) {
+      p[h - hmin] = (int)c.size();
+      for (int k = 1; k <= n - 3; ++k)
+        for (int j = 1; j <= n - 2 - k; ++j) {
+          const int i = h - 2 * j - 3 * k;
+          if (i >= 1 && i + j + k <= n - 1) c.push_back(i | (j << 10) | (k << 20));
+        }
+    }
+    p[hmax - hmin + 1] = (int)c.size();
+    if (g_hp.ptr) cudaFree(g_hp.ptr);
+    if (g_hp.code) cudaFree(g_hp.code);
+    if (cudaMalloc(&g_hp.ptr, p.size() * sizeof(int)) != cudaSuccess) return HHG_ERR_CUDA;
+    if (cudaMalloc(&g_hp.code, std::max<size_t>(c.size(), 1) * sizeof(int)) != cudaSuccess)
+      return HHG_ERR_CUDA;
+    cudaMemcpy(g_hp.ptr, p.data(), p.size() * sizeof(int), cudaMemcpyHostToDevice);
+    if (!c.empty())
+      cudaMemcpy(g_hp.code, c.data(), c.size() * sizeof(int), cudaMemcpyHostToDevice);
+    g_hp.n = n;
+  }
+  *ptr = g_hp.ptr;
+  *code = g_hp.code;
+  return HHG_OK;
+}
+
 static int gs_elem(int var, int64_t n, double *u, const double *fv, const double *kc,
                    const double *coef, int stride, double omega, cudaStream_t st) {
   if (n < 4) return HHG_OK;
@@ -253,8 +288,10 @@ static int gs_elem(int var, int64_t n, double *u, const double *fv, const double
   G.coef_stride = stride;
   G.omega = omega;
   G.lattice = 1;
-  if (var == 0) gs_volume_kernel<0><<<1, 1024, 0, st>>>(G);
-  else gs_volume_kernel<1><<<1, 1024, 0, st>>>(G);
+  int rc = hyperplanes((int)n, &G.hp_ptr, &G.hp_code);
+  if (rc) return rc;
+  if (var == 0) gs_volume_kernel<0><<<1, gs_volume_threads<0>(), 0, st>>>(G);
+  else gs_volume_kernel<1><<<1, gs_volume_threads<1>(), 0, st>>>(G);
   return check("gs_volume_kernel");
 }
 
@@ -390,6 +427,92 @@ int hhg_smooth_surface_level(const hhg_grid *g, const hhg_surface *s,
   return check("gs_surface_kernel");
 }
 
+// surface rows of the smoother, precomputed once: weights + diagonals
+int hhg_smooth_surface_prepare(const hhg_grid *g, const hhg_surface *s,
+                               const hhg_surface_gs *gs, void *stream) {
+  if (s->nrows <= 0) return HHG_OK;
+  SurfGSDesc G{};
+  G.s = surf_desc(g, s);
+  G.shell_gid = reinterpret_cast<const long long *>(g->shell_gid);
+  G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
+  G.ent_col = gs->ent_col;
+  G.ent_val = gs->ent_val;
+  G.row_diag = gs->row_diag;
+  gs_surface_fill_kernel<<<(int)((s->nrows + 127) / 128), 128, 0, S(stream)>>>(G);
+  return check("gs_surface_fill_kernel");
+}
+
+// surface rows of apply / residual from the precomputed rows (+ Dirichlet)
+int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
+                          int flags, const double *u, const double *f, double *out,
+                          void *stream) {
+  const bool res = flags & HHG_FLAG_RESIDUAL;
+  SurfGSDesc G{};
+  G.s = surf_desc(g, s);
+  G.s.u = u;
+  G.s.f = f;
+  G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
+  G.ent_col = gs->ent_col;
+  G.ent_val = gs->ent_val;
+  if (s->nrows > 0) {
+    const int blocks = (int)((s->nrows + 127) / 128);
+    if (res) surface_csr_kernel<true><<<blocks, 128, 0, S(stream)>>>(G, out);
+    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out);
+    int rc = check("surface_csr_kernel");
+    if (rc) return rc;
+  }
+  if (s->ndir > 0) {
+    const int blocks = (int)((s->ndir + 255) / 256);
+    const long long *ids = reinterpret_cast<const long long *>(s->dir_ids);
+    if (res) dirichlet_kernel<true><<<blocks, 256, 0, S(stream)>>>(s->ndir, ids, u, out);
+    else dirichlet_kernel<false><<<blocks, 256, 0, S(stream)>>>(s->ndir, ids, u, out);
+    return check("dirichlet_kernel");
+  }
+  return HHG_OK;
+}
+
+// every level of the surface sweep in one cooperative launch; the grid is
+// sized to the mean level width (a narrow sweep syncs few blocks)
+int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
+                           double omega, double *u, const double *f, void *stream) {
+  if (gs->nlev <= 0) return HHG_OK;
+  SurfGSDesc G{};
+  G.s = surf_desc(g, s);
+  G.s.u = u;
+  G.s.f = f;
+  G.shell_gid = reinterpret_cast<const long long *>(g->shell_gid);
+  G.level_rows = reinterpret_cast<const long long *>(gs->level_rows);
+  G.omega = omega;
+  G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
+  G.ent_col = gs->ent_col;
+  G.ent_val = gs->ent_val;
+  G.row_diag = gs->row_diag;
+  static int max_blocks = 0;
+  if (max_blocks == 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gs_surface_all_kernel, 64, 0);
+    max_blocks = sms * (per > 0 ? per : 1);
+  }
+  // spread each level over many SMs (a single SM's outstanding-miss limit
+  // bounds a level to ~15 us); ~8 rows per 64-thread block
+  long long width = (s->nrows + gs->nlev - 1) / gs->nlev;
+  int blocks = (int)((width + 7) / 8);
+  if (blocks < 8) blocks = 8;
+  if (blocks > max_blocks) blocks = max_blocks;
+  const long long *lp = reinterpret_cast<const long long *>(gs->level_ptr);
+  int nl = (int)gs->nlev;
+  void *args[] = {(void *)&G, (void *)&lp, (void *)&nl};
+  cudaError_t e = cudaLaunchCooperativeKernel((void *)gs_surface_all_kernel, blocks, 64, args,
+                                              0, S(stream));
+  if (e != cudaSuccess) {
+    fprintf(stderr, "hhg_b200: gs_surface_all_kernel: %s\n", cudaGetErrorString(e));
+    return HHG_ERR_CUDA;
+  }
+  return HHG_OK;
+}
+
 int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double omega,
                       double *u, const double *f, void *stream) {
   if (g->n < 4) return HHG_OK;
@@ -409,8 +532,12 @@ int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double
   G.coef_stride = variant == HHG_VAR_NODAL ? 72 : 14;
   G.omega = omega;
   G.lattice = 0;
-  if (variant == HHG_VAR_NODAL) gs_volume_kernel<1><<<g->ntets, 1024, 0, S(stream)>>>(G);
-  else gs_volume_kernel<0><<<g->ntets, 1024, 0, S(stream)>>>(G);
+  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code);
+  if (rc) return rc;
+  if (variant == HHG_VAR_NODAL)
+    gs_volume_kernel<1><<<g->ntets, gs_volume_threads<1>(), 0, S(stream)>>>(G);
+  else
+    gs_volume_kernel<0><<<g->ntets, gs_volume_threads<0>(), 0, S(stream)>>>(G);
   return check("gs_volume_kernel");
 }
 

@@ -126,30 +126,88 @@ __device__ __forceinline__ double scaling_row_fast(double v0, double k0,
   return acc;
 }
 
+// Patch tables as static constexpr members: every index below is a template
+// argument, so the 55-slot element-sum buffer stays in registers (indexing a
+// constexpr array with a loop variable made nvcc materialise the tables in
+// local memory).
+struct Patch {
+  static constexpr int tptr[15] = HHG_TPTR;
+  static constexpr int telem[72] = HHG_TELEM;
+  static constexpr int cse[40][3] = HHG_CSE;
+};
+
+template <int R>
+__device__ __forceinline__ void cse_steps(double (&b)[55]) {
+  if constexpr (R < 40) {
+    constexpr int dst = Patch::cse[R][0], a = Patch::cse[R][1], c = Patch::cse[R][2];
+    b[dst] = dadd(b[a], b[c]);
+    cse_steps<R + 1>(b);
+  }
+}
+
+// s_d = sum over the terms t of direction d of buf[31 + telem[t]] * fac[t],
+// left to right (kernels.py:172-177)
+template <int T, int END, class FAC>
+__device__ __forceinline__ double dir_terms(double s, const double (&b)[55], const FAC &fac) {
+  if constexpr (T < END) {
+    constexpr int slot = 31 + Patch::telem[T];
+    return dir_terms<T + 1, END>(dadd(s, dmul(b[slot], fac[T])), b, fac);
+  } else {
+    return s;
+  }
+}
+
+template <int D, class FAC>
+__device__ __forceinline__ double dir_sum(const double (&b)[55], const FAC &fac) {
+  constexpr int t0 = Patch::tptr[D], t1 = Patch::tptr[D + 1];
+  constexpr int slot = 31 + Patch::telem[t0];
+  return dir_terms<t0 + 1, t1>(dmul(b[slot], fac[t0]), b, fac);
+}
+
+// acc = s_0 (v_0 - v0) + s_1 (v_1 - v0) + ... in direction order
+template <int D, class FAC>
+__device__ __forceinline__ double nodal_acc(double acc, double v0, const double2 (&q)[14],
+                                            const double (&b)[55], const FAC &fac) {
+  if constexpr (D < 14) {
+    const double term = dmul(dir_sum<D>(b, fac), dsub(q[D].x, v0));
+    return nodal_acc<D + 1>(D == 0 ? term : dadd(acc, term), v0, q, b, fac);
+  } else {
+    return acc;
+  }
+}
+
+__device__ __forceinline__ void nodal_buffer(double k0, const double2 (&q)[14],
+                                             double (&b)[55]) {
+  b[0] = k0;
+#pragma unroll
+  for (int d = 0; d < 14; ++d) b[1 + d] = q[d].y;
+  cse_steps<0>(b);
+}
+
 // nodal-integration row, exact reference order (kernels.py:139-189)
 template <class FAC>
 __device__ __forceinline__ double nodal_row_exact(double v0, double k0,
                                                   const double2 (&q)[14],
                                                   const FAC &fac) {
   double b[55];
-  b[0] = k0;
-#pragma unroll
-  for (int d = 0; d < 14; ++d) b[1 + d] = q[d].y;
-#pragma unroll
-  for (int r = 0; r < 40; ++r)
-    b[pt_cse(r, 0)] = dadd(b[pt_cse(r, 1)], b[pt_cse(r, 2)]);
-  double acc = 0.0;
-#pragma unroll
-  for (int d = 0; d < 14; ++d) {
-    const int t0 = pt_tptr(d);
-    double s = dmul(b[31 + pt_telem(t0)], fac[t0]);
-#pragma unroll
-    for (int t = t0 + 1; t < pt_tptr(d + 1); ++t)
-      s = dadd(s, dmul(b[31 + pt_telem(t)], fac[t]));
-    const double term = dmul(s, dsub(q[d].x, v0));
-    acc = (d == 0) ? term : dadd(acc, term);
+  nodal_buffer(k0, q, b);
+  return nodal_acc<0>(0.0, v0, q, b, fac);
+}
+
+// GS form (kernels.py:553-600): acc += s_d u_d, diag -= s_d
+template <int D, class FAC>
+__device__ __forceinline__ void nodal_gs_terms(double &acc, double &diag,
+                                               const double2 (&q)[14],
+                                               const double (&b)[55], const FAC &fac,
+                                               unsigned mask = 0x3fffu) {
+  if constexpr (D < 14) {
+    if (mask >> D & 1) {
+      const double s = dir_sum<D>(b, fac);
+      acc = dadd(acc, dmul(s, q[D].x));
+      diag = dsub(diag, s);
+    }
+    nodal_gs_terms<D + 1>(acc, diag, q, b, fac, mask);
   }
-  return acc;
 }
 
 }  // namespace hhg

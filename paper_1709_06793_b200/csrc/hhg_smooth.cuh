@@ -16,6 +16,7 @@
 #pragma once
 #include "hhg_common.cuh"
 #include "hhg_surface.cuh"
+#include <cooperative_groups.h>
 
 namespace hhg {
 
@@ -34,6 +35,8 @@ struct GSDesc {
   int coef_stride;
   double omega;
   int lattice;                 // 1: per-element lattice arrays
+  const int *hp_ptr;           // [3n-4] hyperplane h = 6 + idx -> point range
+  const int *hp_code;          // [nvol] i | j << 10 | k << 20, by hyperplane
 };
 
 __device__ __forceinline__ double *gs_addr(const GSDesc &D, int t, int i, int j,
@@ -54,8 +57,12 @@ __device__ __forceinline__ double *gs_addr(const GSDesc &D, int t, int i, int j,
   return const_cast<double *>(inner ? g + (i == 0 ? 0 : 1) : g + i);
 }
 
+// block size: the nodal row's 55-slot buffer needs > 64 registers
 template <int VAR>
-__global__ void __launch_bounds__(1024)
+constexpr int gs_volume_threads() { return VAR == 0 ? 512 : 256; }
+
+template <int VAR>
+__global__ void __launch_bounds__(gs_volume_threads<VAR>())
 gs_volume_kernel(GSDesc D) {
   const int t = blockIdx.x;
   const int n = D.n;
@@ -71,27 +78,40 @@ gs_volume_kernel(GSDesc D) {
     __syncthreads();
   }
   const double omega = D.omega;
-  const int J = (n + 1) / 2 + 1;          // bound on points per (h, k)
   const int hmin = 6, hmax = 3 * n - 6;
   const double *kt = D.kc + (long long)t * D.L;
   for (int h = hmin; h <= hmax; ++h) {
-    const int npairs = (n - 3) * J;
-    for (int e = threadIdx.x; e < npairs; e += blockDim.x) {
-      const int k = 1 + e / J;
-      const int jlo0 = h - 2 * k - n + 1;
-      const int jlo = jlo0 > 1 ? jlo0 : 1;
-      const int j = jlo + e % J;
-      const int i = h - 2 * j - 3 * k;
-      if (i < 1 || j > n - 2 - k || i + j + k > n - 1) continue;
-      bool gp;
-      double *up = gs_addr(D, t, i, j, k, gp);
-      const double k0 = kt[lbase(n, k, j) + i];
+    const int ha = D.hp_ptr[h - hmin], hb = D.hp_ptr[h - hmin + 1];
+    for (int e = ha + threadIdx.x; e < hb; e += blockDim.x) {
+      const int code = __ldg(D.hp_code + e);
+      const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+      // 32-bit plane constants of planes k-1, k, k+1 (as the surface rows)
+      const IncPlanes P = inc_planes(n, k);
+      double *ut = D.lattice ? D.u + (long long)t * D.L : D.u + D.vol_start[t];
+      const double *gt = D.ghost + (long long)t * D.S;
+      double *up;
+      if (D.lattice) {
+        up = ut + inc_koff(P, 1, i, j);
+      } else {
+        int off;
+        inc_voff(P, 1, n, i, j, k, off);              // interior point
+        up = ut + off;
+      }
+      const double k0 = kt[inc_koff(P, 1, i, j)];
       double2 q[14];
 #pragma unroll
       for (int d = 0; d < 14; ++d) {
-        const int qi = i + c_dirs[d][0], qj = j + c_dirs[d][1], qk = k + c_dirs[d][2];
-        q[d].x = *gs_addr(D, t, qi, qj, qk, gp);
-        q[d].y = kt[lbase(n, qk, qj) + qi];
+        const int dk = c_dirs_h(d, 2);
+        const int qi = i + c_dirs_h(d, 0), qj = j + c_dirs_h(d, 1), qk = k + dk;
+        const int ko = inc_koff(P, dk + 1, qi, qj);
+        if (D.lattice) {
+          q[d].x = ut[ko];
+        } else {
+          int off;
+          const bool in = inc_voff(P, dk + 1, n, qi, qj, qk, off);
+          q[d].x = in ? ut[off] : gt[off];
+        }
+        q[d].y = kt[ko];
       }
       double acc = 0.0, diag = 0.0;
       if (VAR == 0) {
@@ -103,25 +123,11 @@ gs_volume_kernel(GSDesc D) {
         }
       } else {
         double b[55];
-        b[0] = k0;
-#pragma unroll
-        for (int d = 0; d < 14; ++d) b[1 + d] = q[d].y;
-#pragma unroll
-        for (int r = 0; r < 40; ++r)
-          b[pt_cse(r, 0)] = dadd(b[pt_cse(r, 1)], b[pt_cse(r, 2)]);
-#pragma unroll
-        for (int d = 0; d < 14; ++d) {
-          const int t0 = pt_tptr(d);
-          double s = dmul(b[31 + pt_telem(t0)], sfac[t0]);
-#pragma unroll
-          for (int tt = t0 + 1; tt < pt_tptr(d + 1); ++tt)
-            s = dadd(s, dmul(b[31 + pt_telem(tt)], sfac[tt]));
-          acc = dadd(acc, dmul(s, q[d].x));
-          diag = dsub(diag, s);
-        }
+        nodal_buffer(k0, q, b);
+        nodal_gs_terms<0>(acc, diag, q, b, sfac);
       }
       if (diag == 0.0) atomicOr(&g_status, 1);
-      const long long c = lbase(n - 4, k - 1, j - 1) + i - 1;
+      const long long c = lbase32(n - 4, k - 1, j - 1) + i - 1;
       const double fv = D.lattice ? D.f[(long long)t * D.nvol + c]
                                   : D.f[D.vol_start[t] + c];
       *up = dadd(dmul(dsub(1.0, omega), *up), ddiv(dmul(omega, dsub(fv, acc)), diag));
@@ -137,6 +143,11 @@ struct SurfGSDesc {
   const long long *level_rows;  // row indices (into s.rows) of this level
   long long count;
   double omega;
+  // precomputed rows (hhg_smooth_surface_prepare): neighbour ids and
+  // weights in the exact accumulation order, and the diagonals
+  const long long *ent_ptr;
+  int *ent_col;
+  double *ent_val, *row_diag;
 };
 
 __device__ __forceinline__ long long point_gid(const SurfDesc &D,
@@ -151,11 +162,8 @@ __device__ __forceinline__ long long point_gid(const SurfDesc &D,
   return shell_gid[inner ? off + (i == 0 ? 0 : 1) : off + i];
 }
 
-__global__ void gs_surface_kernel(SurfGSDesc G) {
-  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (e >= G.count) return;
+__device__ __forceinline__ void gs_surface_row(const SurfGSDesc &G, long long r) {
   const SurfDesc &D = G.s;
-  const long long r = G.level_rows[e];
   const long long gid = D.rows[r];
   double *u = const_cast<double *>(D.u);
   const bool nodal = D.row_nodal[r] != 0;
@@ -173,7 +181,7 @@ __global__ void gs_surface_kernel(SurfGSDesc G) {
     for (int d = 0; d < 14; ++d) {
       if (mask >> d & 1) {
         const int qi = i + c_dirs[d][0], qj = j + c_dirs[d][1], qk = k + c_dirs[d][2];
-        q[d].x = u[point_gid(D, G.shell_gid, t, qi, qj, qk)];
+        q[d].x = __ldcg(u + point_gid(D, G.shell_gid, t, qi, qj, qk));
         q[d].y = kt[lbase(D.n, qk, qj) + qi];
       } else {
         q[d].x = 0.0;
@@ -192,28 +200,180 @@ __global__ void gs_surface_kernel(SurfGSDesc G) {
     } else {
       const double *fac = D.pfac + ((long long)t * 14 + cls) * 72;
       double b[55];
-      b[0] = k0;
-#pragma unroll
-      for (int d = 0; d < 14; ++d) b[1 + d] = q[d].y;
-#pragma unroll
-      for (int rr = 0; rr < 40; ++rr)
-        b[pt_cse(rr, 0)] = dadd(b[pt_cse(rr, 1)], b[pt_cse(rr, 2)]);
-#pragma unroll
-      for (int d = 0; d < 14; ++d) {
-        if (!(mask >> d & 1)) continue;
-        const int t0 = pt_tptr(d);
-        double s = dmul(b[31 + pt_telem(t0)], fac[t0]);
-#pragma unroll
-        for (int tt = t0 + 1; tt < pt_tptr(d + 1); ++tt)
-          s = dadd(s, dmul(b[31 + pt_telem(tt)], fac[tt]));
-        acc = dadd(acc, dmul(s, q[d].x));
-        diag = dsub(diag, s);
-      }
+      nodal_buffer(k0, q, b);
+      nodal_gs_terms<0>(acc, diag, q, b, fac, mask);
     }
   }
   if (diag == 0.0) atomicOr(&g_status, 1);
   const double om = G.omega;
-  u[gid] = dadd(dmul(dsub(1.0, om), u[gid]), ddiv(dmul(om, dsub(D.f[gid], acc)), diag));
+  u[gid] = dadd(dmul(dsub(1.0, om), __ldcg(u + gid)), ddiv(dmul(om, dsub(D.f[gid], acc)), diag));
+}
+
+
+// setup: the weights of every surface row in the order gs_surface_row
+// accumulates them (incidence, then direction), and -sum of them as the
+// diagonal — computed once on the device (k is fixed), bitwise the values
+// gs_surface_row would recompute in every sweep
+template <int D, class FAC>
+__device__ __forceinline__ void nodal_row_weights(double &diag, double *&val,
+                                                  const double (&b)[55], const FAC &fac,
+                                                  unsigned mask) {
+  if constexpr (D < 14) {
+    if (mask >> D & 1) {
+      const double sd = dir_sum<D>(b, fac);
+      *val++ = sd;
+      diag = dsub(diag, sd);
+    }
+    nodal_row_weights<D + 1>(diag, val, b, fac, mask);
+  }
+}
+
+__global__ void gs_surface_fill_kernel(SurfGSDesc G) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const SurfDesc &D = G.s;
+  if (r >= D.nrows) return;
+  const bool nodal = D.row_nodal[r] != 0;
+  double diag = 0.0;
+  double *val = G.ent_val + G.ent_ptr[r];
+  int *col = G.ent_col + G.ent_ptr[r];
+  for (int x = D.inc_ptr[r]; x < D.inc_ptr[r + 1]; ++x) {
+    const int t = D.inc_tet[x];
+    const int code = D.inc_code[x];
+    const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+    const int cls = D.inc_cls[x];
+    const unsigned mask = c_cls_dirmask[cls];
+    const double *kt = D.kc + (long long)t * D.L;
+    const double k0 = kt[lbase(D.n, k, j) + i];
+    double2 q[14];
+#pragma unroll
+    for (int d = 0; d < 14; ++d) {
+      q[d].x = 0.0;
+      q[d].y = 0.0;
+      if (mask >> d & 1) {
+        const int qi = i + c_dirs[d][0], qj = j + c_dirs[d][1], qk = k + c_dirs[d][2];
+        q[d].y = kt[lbase(D.n, qk, qj) + qi];
+        *col++ = (int)point_gid(D, G.shell_gid, t, qi, qj, qk);
+      }
+    }
+    if (!nodal) {
+      const double *sh = D.psh + ((long long)t * 14 + cls) * 14;
+#pragma unroll
+      for (int d = 0; d < 14; ++d)
+        if (mask >> d & 1) {
+          const double sd = dmul(dadd(k0, q[d].y), sh[d]);
+          *val++ = sd;
+          diag = dsub(diag, sd);
+        }
+    } else {
+      const double *fac = D.pfac + ((long long)t * 14 + cls) * 72;
+      double b[55];
+      nodal_buffer(k0, q, b);
+      nodal_row_weights<0>(diag, val, b, fac, mask);
+    }
+  }
+  G.row_diag[r] = diag;
+}
+
+// one GS row from the precomputed list: acc = sum w u (stored order)
+__device__ __forceinline__ void gs_surface_row_csr(const SurfGSDesc &G, long long r) {
+  const SurfDesc &D = G.s;
+  const long long gid = D.rows[r];
+  double *u = const_cast<double *>(D.u);
+  double acc = 0.0;
+  const long long e1 = G.ent_ptr[r + 1];
+  long long e = G.ent_ptr[r];
+  // loads batched 8 at a time (independent), accumulation still in order
+  for (; e + 8 <= e1; e += 8) {
+    int cl[8];
+    double w[8], x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) cl[m] = __ldg(G.ent_col + e + m);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      w[m] = __ldg(G.ent_val + e + m);
+      x[m] = __ldcg(u + (unsigned)cl[m]);
+    }
+#pragma unroll
+    for (int m = 0; m < 8; ++m) acc = dadd(acc, dmul(w[m], x[m]));
+  }
+  for (; e < e1; ++e)
+    acc = dadd(acc, dmul(__ldg(G.ent_val + e), __ldcg(u + (unsigned)__ldg(G.ent_col + e))));
+  const double diag = G.row_diag[r];
+  if (diag == 0.0) atomicOr(&g_status, 1);
+  const double om = G.omega;
+  u[gid] = dadd(dmul(dsub(1.0, om), __ldcg(u + gid)), ddiv(dmul(om, dsub(D.f[gid], acc)), diag));
+}
+
+// apply / residual of the surface rows from the precomputed weights:
+// part = sum_d w_d (v_d - v0) per incidence (direction order), row = sum of
+// parts (incidence order) — the association of surface_partial_kernel +
+// surface_reduce_kernel, with w_d = (k0 + k_d) * psh_d (or the nodal s_d)
+// read instead of recomputed
+template <bool RES>
+__global__ void surface_csr_kernel(SurfGSDesc G, double *out) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const SurfDesc &D = G.s;
+  if (r >= D.nrows) return;
+  const long long gid = D.rows[r];
+  const double v0 = D.u[gid];
+  long long e = G.ent_ptr[r];
+  double row = 0.0;
+  for (int x = D.inc_ptr[r]; x < D.inc_ptr[r + 1]; ++x) {
+    const int cnt = __popc(c_cls_dirmask[D.inc_cls[x]]);   // 1..12 entries
+    int cl[12];
+    double w[12], vq[12];
+#pragma unroll
+    for (int m = 0; m < 12; ++m)
+      if (m < cnt) cl[m] = __ldg(G.ent_col + e + m);
+#pragma unroll
+    for (int m = 0; m < 12; ++m)
+      if (m < cnt) {
+        w[m] = __ldg(G.ent_val + e + m);
+        vq[m] = __ldg(D.u + (unsigned)cl[m]);
+      }
+    double part = dmul(w[0], dsub(vq[0], v0));
+#pragma unroll
+    for (int m = 1; m < 12; ++m)
+      if (m < cnt) part = dadd(part, dmul(w[m], dsub(vq[m], v0)));
+    e += cnt;
+    row = dadd(row, part);
+  }
+  if (RES) row = dsub(D.f[gid], row);
+  out[gid] = row;
+}
+
+__global__ void gs_surface_kernel(SurfGSDesc G) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < G.count) gs_surface_row(G, G.level_rows[e]);   // recomputing form
+}
+
+// narrow sweeps: one CTA walks all levels, a block barrier between levels
+__global__ void __launch_bounds__(1024)
+gs_surface_block_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
+  for (int lv = 0; lv < nlev; ++lv) {
+    const long long a = level_ptr[lv], b = level_ptr[lv + 1];
+    for (long long e = a + threadIdx.x; e < b; e += blockDim.x)
+      gs_surface_row_csr(G, G.level_rows[e]);
+    __syncthreads();
+  }
+}
+
+// all levels in one cooperative launch: rows of a level are spread over the
+// grid, a grid-wide barrier (with its memory fence) separates the levels;
+// neighbour values are read with ld.global.cg so no stale L1 copy survives
+// a level boundary
+__global__ void __launch_bounds__(64)
+gs_surface_all_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  // row m of a level goes to block m % gridDim: a narrow level still
+  // spreads over all participating SMs
+  const long long tid = threadIdx.x * (long long)gridDim.x + blockIdx.x;
+  const long long nth = (long long)gridDim.x * blockDim.x;
+  for (int lv = 0; lv < nlev; ++lv) {
+    const long long a = level_ptr[lv], b = level_ptr[lv + 1];
+    for (long long e = a + tid; e < b; e += nth) gs_surface_row_csr(G, G.level_rows[e]);
+    grid.sync();
+  }
 }
 
 }  // namespace hhg

@@ -666,27 +666,52 @@ volume_kernel_mirror(VolDesc D) {
   }
   __syncthreads();
 
+  // Staging slots carry their offsets from plane to plane: with
+  // T2(m) = (m+1)(m+2)/2 the lattice offset of (i, j, p+1) is that of
+  // (i, j, p) plus T2(n-p) - j, the volume-block offset grows by
+  // T2(n-3-p) - (j-1), the ghost offset by 3(n-p) - [j > 0]; only these
+  // uniform deltas are formed per plane.
+  struct IncSlot {
+    int ko, vo, go;   // lattice, volume-block, ghost offsets at the next plane
+    int pmax;         // last plane containing the point (i + j + p <= n)
+    int ij;           // i | j << 16
+  };
+  IncSlot sl_[NSLOT];
+#pragma unroll
+  for (int m = 0; m < NSLOT; ++m) {
+    const int e = threadIdx.x + m * NT;
+    const int r = e / VOL_COLS, cc = e - r * VOL_COLS;
+    const int si = i0 - 1 + cc, sj = j0 - 1 + r;
+    sl_[m].ij = si | (sj << 16);
+    sl_[m].pmax = (e < ROWS * VOL_COLS) ? n - si - sj : -1;
+    sl_[m].ko = sj * (n + 1) - sj * (sj - 1) / 2 + si;                   // plane 0
+    sl_[m].vo = (sj - 1) * (n - 3) - (sj - 1) * (sj - 2) / 2 + si - 1;    // plane 1
+    sl_[m].go = sl_[m].ko;                                               // plane 0
+  }
+  const int t2n = (n + 1) * (n + 2) / 2;
   auto produce = [&](int p) {
     const int sl = p % NS;
     if (p >= NS) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
-    const PlaneConst P = plane_const(n, p);
-    const unsigned off = (unsigned)sl * PLANE_BYTES;
+    const unsigned off = ring_s + (unsigned)sl * PLANE_BYTES;
 #pragma unroll
     for (int m = 0; m < NSLOT; ++m) {
-      const int e = threadIdx.x + m * NT;
-      if (e < ROWS * VOL_COLS) {
-        Slot S;
-        const int r = e / VOL_COLS, cc = e - r * VOL_COLS;
-        S.live = true;
-        S.i = i0 - 1 + cc;
-        S.j = j0 - 1 + r;
-        S.jk = -S.j * (S.j - 1) / 2 + S.i;
-        S.ji = -(S.j - 1) * (S.j - 2) / 2 + S.i - 1;
-        S.g0 = S.j * (n + 1) - S.j * (S.j - 1) / 2 + S.i;
-        S.gin = (S.j == 0) ? S.i : (n + 1) + 2 * (S.j - 1) + (S.i == 0 ? 0 : 1);
-        S.dst = ring_s + (unsigned)e * sizeof(double2);
-        stage_slot<SRC>(T, S, P, n, p, off);
+      IncSlot &S = sl_[m];
+      const int si = S.ij & 0xffff, sj = S.ij >> 16;
+      if (p <= S.pmax) {
+        const bool interior = p >= 1 && si >= 1 && sj >= 1 && p < S.pmax;
+        const double *vs = interior ? at(T.v, S.vo) : at(T.g, S.go);
+        const double *ks = at(T.k, S.ko);
+        const unsigned d = off + (unsigned)(threadIdx.x + m * NT) * sizeof(double2);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(vs));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 8), "l"(ks));
       }
+      // advance to plane p + 1
+      S.ko += (n - p + 1) * (n - p) / 2 + (n - p + 1) - sj;   // T2(n - p) - j
+      if (p >= 1) S.vo += (n - 2 - p) * (n - 1 - p) / 2 - (sj - 1);  // T2(n-3-p) - (j-1)
+      if (p == 0)
+        S.go = t2n + (sj == 0 ? si : n + 2 * (sj - 1) + (si > 0 ? 1 : 0));
+      else
+        S.go += 3 * (n - p) - (sj > 0 ? 1 : 0);
     }
     mbar_arrive_cp_async(full0 + 8 * sl);
   };

@@ -201,6 +201,15 @@ class SurfaceTables:
         level_ptr = np.searchsorted(level[order], np.arange(nlev + 1))
         return order.astype(np.int64), level_ptr.astype(np.int64), int(nlev)
 
+    def entry_ptr(self):
+        """Row offsets of the precomputed surface rows: one entry per
+        (incidence, in-element direction), in accumulation order."""
+        _, dir_inside = class_element_masks()
+        per_inc = dir_inside.sum(axis=1)[self.inc_cls]
+        row_of_inc = np.repeat(np.arange(len(self.rows)), np.diff(self.inc_ptr))
+        cnt = np.bincount(row_of_inc, weights=per_inc, minlength=len(self.rows))
+        return np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+
 
 def partial_tables(op_tables):
     """Stack per-element partial stencils (psh, pfac)."""
@@ -281,10 +290,38 @@ class DeviceSurface:
         self.desc = d
         self.ref = ctypes.byref(d)
         self._levels = None
+        self._csr = None
 
-    def levels(self):
+    def csr(self, dg):
+        """Precomputed surface rows (neighbour ids + weights, filled on the
+        device once; k does not change) for apply, residual and smoothing."""
+        if self._csr is None:
+            from ._lib import HhgSurfaceGS, check
+            torch = require_cuda()
+            ent_ptr = self.st.entry_ptr()
+            nent = int(ent_ptr[-1])
+            keep = [torch.as_tensor(ent_ptr, device="cuda"),
+                    torch.empty(max(nent, 1), dtype=torch.int32, device="cuda"),
+                    torch.empty(max(nent, 1), dtype=torch.float64, device="cuda"),
+                    torch.empty(max(len(self.st.rows), 1), dtype=torch.float64, device="cuda")]
+            d = HhgSurfaceGS()
+            d.ent_ptr, d.ent_col = keep[0].data_ptr(), keep[1].data_ptr()
+            d.ent_val, d.row_diag = keep[2].data_ptr(), keep[3].data_ptr()
+            check(lib.hhg_smooth_surface_prepare(dg.ref, self.ref, ctypes.byref(d),
+                                                 torch.cuda.current_stream().cuda_stream),
+                  "smooth_surface_prepare")
+            self._csr = {"desc": d, "ref": ctypes.byref(d), "keep": keep}
+        return self._csr
+
+    def gs_tables(self, dg):
+        """Level schedule of the surface smoother on top of csr()."""
+        c = self.csr(dg)
         if self._levels is None:
             torch = require_cuda()
             order, ptr, nlev = self.st.gs_levels()
-            self._levels = (torch.as_tensor(order, device="cuda"), ptr, nlev)
-        return self._levels
+            keep = [torch.as_tensor(order, device="cuda"), torch.as_tensor(ptr, device="cuda")]
+            c["desc"].level_rows, c["desc"].level_ptr = keep[0].data_ptr(), keep[1].data_ptr()
+            c["desc"].nlev = nlev
+            c["keep"] += keep
+            self._levels = nlev
+        return {"ref": c["ref"], "nlev": self._levels}

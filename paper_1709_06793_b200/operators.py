@@ -59,7 +59,7 @@ class Operator:
     """One operator variant bound to a grid and coefficient, on the GPU."""
 
     def __init__(self, grid, variant: str, coeff=None, hybrid_nodal=frozenset(),
-                 fast=False):
+                 fast=False, surface_mode="csr"):
         if variant not in VARIANTS:
             raise ValueError(f"unknown variant {variant!r}")
         if variant == "stored":
@@ -75,6 +75,9 @@ class Operator:
         self.ma2_marked = None
         self._stored = None
         self.fast = bool(fast)
+        if surface_mode not in ("csr", "matrix-free"):
+            raise ValueError("surface_mode must be 'csr' or 'matrix-free'")
+        self.surface_mode = surface_mode
         if variant == "const":
             self.const_value = 1.0 if coeff is None else float(coeff)
             if self.const_value <= 0:
@@ -241,11 +244,20 @@ class Operator:
         check(lib.hhg_volume_apply(dg.ref, self._vol_variant(), flags,
                                    D["coef"].data_ptr(), wp, du.data_ptr(), fp,
                                    out.data_ptr(), st), "volume_apply")
-        check(lib.hhg_surface_apply(dg.ref, ds.ref, 0, flags & _lib.FLAG_RESIDUAL,
-                                    du.data_ptr(), fp, out.data_ptr(), st),
-              "surface_apply")
+        self._surface(dg, ds, flags & _lib.FLAG_RESIDUAL, du, fp, out, st)
         self._count()
         return out
+
+    def _surface(self, dg, ds, res_flag, du, fp, out, st):
+        """Surface + Dirichlet rows: from the precomputed rows when built
+        (setup on first use, `surface_mode="csr"`), else matrix-free."""
+        if self.surface_mode == "csr":
+            c = ds.csr(dg)
+            check(lib.hhg_surface_apply_csr(dg.ref, ds.ref, c["ref"], res_flag, du.data_ptr(),
+                                            fp, out.data_ptr(), st), "surface_apply_csr")
+        else:
+            check(lib.hhg_surface_apply(dg.ref, ds.ref, 0, res_flag, du.data_ptr(), fp,
+                                        out.data_ptr(), st), "surface_apply")
 
     # -- host-buffer pipeline ---------------------------------------------------
     def _pipeline(self, groups=8):
@@ -329,8 +341,7 @@ class Operator:
                 a, b = int(vs[P["bounds"][g]]), int(vs[P["bounds"][g + 1] - 1] + nv)
                 with torch.cuda.stream(d2h):
                     hout[a:b].copy_(out[a:b], non_blocking=True)
-        check(lib.hhg_surface_apply(dg.ref, ds.ref, 0, 0, du.data_ptr(), None,
-                                    out.data_ptr(), cs), "surface_apply")
+        self._surface(dg, ds, 0, du, None, out, cs)
         e = torch.cuda.Event()
         e.record(comp)
         d2h.wait_event(e)
@@ -363,20 +374,17 @@ class Operator:
         D = self._device()
         dg, ds = D["grid"], D["surf"]
         st = self._stream()
-        order, ptr, nlev = ds.levels()
+        gs = ds.gs_tables(dg)
         src = getattr(self, "source_variant", self.variant)
         if src == "nodal":
             var, coef = _lib.VAR["nodal"], D["coef"] if self._stored is None else D["fac"]
         else:
             var, coef = _lib.VAR["scaling"], D["sh"]
         lib.hhg_status_reset()
-        base = order.data_ptr()
         for _ in range(sweeps):
-            for lv in range(nlev):
-                a, b = int(ptr[lv]), int(ptr[lv + 1])
-                check(lib.hhg_smooth_surface_level(dg.ref, ds.ref, base + 8 * a, b - a,
-                                                   float(omega), du.data_ptr(),
-                                                   df.data_ptr(), st), "smooth_surface")
+            check(lib.hhg_smooth_surface_all(dg.ref, ds.ref, gs["ref"], float(omega),
+                                             du.data_ptr(), df.data_ptr(), st),
+                  "smooth_surface")
             check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
             check(lib.hhg_smooth_volume(dg.ref, var, coef.data_ptr(), float(omega),
                                         du.data_ptr(), df.data_ptr(), st), "smooth_volume")

@@ -266,3 +266,20 @@ def test_large_grid_algebraic_properties(cuda):
     s1 = torch.dot(y, Ax * free).item()
     s2 = torch.dot(x, Ay * free).item()
     assert abs(s1 - s2) <= 1e-10 * abs(s1)
+
+
+@pytest.mark.parametrize("name", ["scaling", "nodal", "hybrid:wv+we"])
+def test_surface_modes_agree_bitwise(cuda, name):
+    """Precomputed surface rows (default) and the matrix-free surface kernels
+    perform the same IEEE operations in the same order."""
+    grid = M.RefinedGrid(case_mesh("c3"), 4)
+    kf = sample_nodal(k_c3(), grid)
+    hn, v = frozenset(), name
+    if name.startswith("hybrid:"):
+        hn, v = parse_hybrid_set(name.split(":", 1)[1]), "hybrid"
+    u = np.random.default_rng(9).uniform(-1, 1, grid.n_nodes)
+    f = np.random.default_rng(10).uniform(-1, 1, grid.n_nodes)
+    a = Operator(grid, v, kf, hybrid_nodal=hn)
+    b = Operator(grid, v, kf, hybrid_nodal=hn, surface_mode="matrix-free")
+    assert np.array_equal(a.apply(u), b.apply(u))
+    assert np.array_equal(a.residual(u, f), b.residual(u, f))

@@ -53,6 +53,6 @@ for _ in range(5):
     op.smooth_device(du, df, 1)
 torch.cuda.synchronize()
 out["c4_smooth_sweep_ms"] = (time.perf_counter() - t0) / 5 * 1e3
-nlev = op._device()["surf"].levels()[2]
+nlev = op._device()["surf"].gs_tables(op._device()["grid"])["nlev"]
 out["c4_surface_gs_levels"] = nlev
 print(json.dumps(out))
