@@ -253,8 +253,8 @@ def run_own(args):
                        "macro_tets_per_gpu": ntets, "dofs_per_gpu": int(grid.n_nodes),
                        "volume_dofs_per_gpu": int(nvol_rank), "variant": args.variant,
                        "arithmetic": "fast-fma" if args.fast else
-                       ("bitwise-reference-order, mirror edge reuse" if op._mirror
-                        else "bitwise-reference-order"),
+                       ("bitwise-reference-order, mirror edge reuse"
+                        if op._vol_flags() & 4 else "bitwise-reference-order"),
                        "parallelism": f"macro-tet slabs x{world}",
                        "l2": "inputs larger than L2 (2.2 GB per vector)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
@@ -265,7 +265,8 @@ def run_own(args):
             "e2e": {"value": round(total_dofs / (e2e * 1e-3) / 1e9, 4), "unit": "GDoF/s",
                     "ms_per_step": round(e2e, 2), "h2d_bytes_per_step": 8 * grid.n_nodes,
                     "d2h_bytes_per_step": 8 * grid.n_nodes},
-            "gpu_launches": args.steps * 4,
+            "gpu_launches": args.steps * (4 if imap is None else 4),
+            "all_rows_gdofs": round(grid.n_nodes * world / (ms * 1e-3) / 1e9, 3),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "setup_s": round(t_setup, 1),

@@ -22,7 +22,7 @@ using namespace hhg;
 #define HHG_VOL_W 4
 #endif
 #ifndef HHG_VOL_NS
-#define HHG_VOL_NS 8
+#define HHG_VOL_NS 6
 #endif
 
 #ifndef HHG_VOL_MINB
