@@ -221,6 +221,58 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s,
 int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef,
                       double omega, double *u, const double *f, void *stream);
 
+/* ---------------------------------------------------------------------
+ * (3) tensor-coefficient operators, M = 6 component fields
+ *     (coefficients.py:120-200, TENSOR_DIRS_3D).  km is float64[M][L] per
+ *     element (device), shm float64[M][14], fac float64[M][72]; any other
+ *     M returns HHG_ERR_ARG.
+ * --------------------------------------------------------------------- */
+
+/* replaces kernels.apply_scaling_tensor_3d(n, base, v, km, shm, out),
+ * kernels.py:192-232 (M = km.shape[0] passed explicitly) */
+int hhg_apply_scaling_tensor_3d(int64_t n, const int64_t *base, const double *v,
+                                const double *km, int64_t M, const double *shm,
+                                double *out, void *stream);
+
+/* replaces kernels.apply_nodal_tensor_3d(n, base, v, km, sched, sums, fac,
+ * tptr, telem, out), kernels.py:235-286 (host tables as for
+ * hhg_apply_nodal_3d) */
+int hhg_apply_nodal_tensor_3d(int64_t n, const int64_t *base, const double *v,
+                              const double *km, int64_t M, const int64_t *sched,
+                              int64_t nsched, const int64_t *sums, const double *fac,
+                              const int64_t *tptr, const int64_t *telem, double *out,
+                              void *stream);
+
+/* replaces kernels.gs_scaling_tensor_3d(n, base, u, fv, km, shm, omega),
+ * kernels.py:603-640 (hyperplane wavefronts, bitwise the sequential sweep) */
+int hhg_gs_scaling_tensor_3d(int64_t n, const int64_t *base, double *u,
+                             const double *fv, const double *km, int64_t M,
+                             const double *shm, double omega, void *stream);
+
+/* replaces kernels.gs_nodal_tensor_3d(...), kernels.py:643-702 */
+int hhg_gs_nodal_tensor_3d(int64_t n, const int64_t *base, double *u,
+                           const double *fv, const double *km, int64_t M,
+                           const int64_t *sched, int64_t nsched, const int64_t *sums,
+                           const double *fac, const int64_t *tptr,
+                           const int64_t *telem, double omega, void *stream);
+
+/* batched volume rows of the tensor operators (Operator._run_volume tensor
+ * branch, operators.py:406-426): variant HHG_VAR_SCALING or HHG_VAR_NODAL;
+ * km [ntets][M][L], coef [ntets][M][14 | 72]; flags: HHG_FLAG_RESIDUAL */
+int hhg_tensor_volume_apply(const hhg_grid *g, int variant, int flags, int M,
+                            const double *km, const double *coef, const double *u,
+                            const double *f, double *out, void *stream);
+int hhg_tensor_smooth_volume(const hhg_grid *g, int variant, int M, const double *km,
+                             const double *coef, double omega, double *u,
+                             const double *f, void *stream);
+/* surface rows of the tensor operators (operators.py:277-327 tensor branch):
+ * s->psh is [ntets][M][14][14], s->pfac [ntets][M][14][72]; fills the same
+ * precomputed rows hhg_smooth_surface_prepare fills for scalar k, so
+ * hhg_surface_apply_csr / hhg_smooth_surface_all serve both */
+int hhg_tensor_surface_prepare(const hhg_grid *g, const hhg_surface *s,
+                               const hhg_surface_gs *gs, int M, const double *km,
+                               void *stream);
+
 /* HOST helper: level schedule of the surface Gauss-Seidel (see .cu) */
 int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr,
                        const int64_t *dep_idx, int64_t *level);

@@ -24,10 +24,11 @@ _LOCAL_EDGES = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
 _OPP_FACE = ((1, 2, 3), (0, 2, 3), (0, 1, 3), (0, 1, 2))
 
 
-def stiffness(verts):
+def stiffness(verts, cc=None):
     """P1 stiffness of a batch of tetrahedra (m, 4, 3) from face normals:
     grad(lambda_i) = N_i / (N_i . (x_i - x_f)) with N_i the normal of the
-    face opposite vertex i and x_f any vertex of that face."""
+    face opposite vertex i and x_f any vertex of that face.  With a constant
+    3x3 tensor ``cc`` the entries are vol * grad_i . cc grad_j."""
     verts = np.asarray(verts, dtype=np.float64)
     m = verts.shape[0]
     grads = np.empty((m, 4, 3))
@@ -37,7 +38,29 @@ def stiffness(verts):
         grads[:, i] = N / h[:, None]
     e1, e2, e3 = (verts[:, q] - verts[:, 0] for q in (1, 2, 3))
     vol = np.abs(np.einsum("md,md->m", e1, np.cross(e2, e3))) / 6.0
-    return np.einsum("mid,mjd->mij", grads, grads) * vol[:, None, None]
+    if cc is None:
+        return np.einsum("mid,mjd->mij", grads, grads) * vol[:, None, None]
+    return np.einsum("mid,de,mje->mij", grads, np.asarray(cc), grads) * vol[:, None, None]
+
+
+def _tensor_element_matrices(coeff, t, lidx, verts, form):
+    """Sum over the M components of the factored component matrices
+    (oracle.py:90-110): k_m rides on grad (m = 0) or on c_m . grad."""
+    A = None
+    for m, fld in enumerate(coeff.fields):
+        kel = fld.values[t][lidx]
+        A_m = stiffness(verts) if m == 0 else stiffness(
+            verts, np.outer(coeff.dirs[m], coeff.dirs[m]))
+        if form == "nodal":
+            part = kel.mean(axis=1)[:, None, None] * A_m
+        else:
+            part = 0.5 * (kel[:, :, None] + kel[:, None, :]) * A_m
+        A = part if A is None else A + part
+    if form != "nodal":
+        idx = np.arange(4)
+        A[:, idx, idx] = 0.0
+        A[:, idx, idx] = -A.sum(axis=2)
+    return A
 
 
 def _factor(kel, A_hat, form):
@@ -67,7 +90,17 @@ def assemble_global(grid, variant, coeff=None, hybrid_nodal=frozenset(), reduced
     for t in range(grid.macro.n_elements):
         ids = grid.elem_gidx[t][lidx]
         A_hat = stiffness(grid.node_coords[ids])
-        if variant == "const":
+        if hasattr(coeff, "fields"):                     # tensor coefficient
+            verts = grid.node_coords[ids]
+            if variant == "hybrid":
+                An = _tensor_element_matrices(coeff, t, lidx, verts, "nodal")
+                As = _tensor_element_matrices(coeff, t, lidx, verts, "scaling")
+                use = np.isin(grid.node_kind[ids], [int(k) for k in hybrid_nodal])
+                A = np.where(use[:, :, None], An, As)
+            else:
+                A = _tensor_element_matrices(coeff, t, lidx, verts,
+                                             "nodal" if variant == "nodal" else "scaling")
+        elif variant == "const":
             A = (1.0 if coeff is None else float(coeff)) * A_hat
         else:
             kel = coeff.values[t][lidx]
@@ -125,10 +158,19 @@ class CpuOperator:
         self.grid, self.variant, self.coeff = grid, variant, coeff
         ne = grid.macro.n_elements
         self.env = environment(3)
-        self.sh = sh if sh is not None else [reference_stencil(grid, t)[1] / 2.0
-                                             for t in range(ne)]
-        self.fac = fac if fac is not None else (
-            [nodal_factors(grid, t) for t in range(ne)] if variant == "nodal" else None)
+        self.tensor = hasattr(coeff, "fields")
+        if self.tensor:
+            from paper_1709_06793_b200.reference_stencils import tensor_tables
+            tabs = [tensor_tables(grid, t, coeff.dirs) for t in range(ne)]
+            self.sh = [a for a, _ in tabs]
+            self.fac = [b for _, b in tabs]
+            self.km = [np.ascontiguousarray([f.values[t] for f in coeff.fields])
+                       for t in range(ne)]
+        else:
+            self.sh = sh if sh is not None else [reference_stencil(grid, t)[1] / 2.0
+                                                 for t in range(ne)]
+            self.fac = fac if fac is not None else (
+                [nodal_factors(grid, t) for t in range(ne)] if variant == "nodal" else None)
         surf = np.zeros(grid.n_nodes, dtype=bool)
         surf[:grid.n_surface_nodes] = True
         surf &= ~grid.dirichlet_mask
@@ -144,6 +186,13 @@ class CpuOperator:
     def _volume(self, t, uloc):
         g, n = self.grid, self.grid.n
         base = g.lat.base
+        if self.tensor:
+            e = self.env
+            if self.variant == "nodal":
+                return ok.apply_nodal_tensor_3d(n, base, uloc, self.km[t], e.cse_schedule,
+                                                e.cse_sums, self.fac[t], e.term_ptr,
+                                                e.term_elem)
+            return ok.apply_scaling_tensor_3d(n, base, uloc, self.km[t], self.sh[t])
         if self.variant == "nodal":
             e = self.env
             return ok.apply_nodal_3d(n, base, uloc, self.coeff.values[t], e.cse_schedule,
@@ -181,7 +230,16 @@ class CpuOperator:
                 uloc = np.ascontiguousarray(u[g.elem_gidx[t]])
                 s0 = g.vol_start[t]
                 fv = f[s0:s0 + self.nvol]
-                if self.variant == "nodal":
+                if self.tensor:
+                    e = self.env
+                    if self.variant == "nodal":
+                        ok.gs_nodal_tensor_3d(n, g.lat.base, uloc, fv, self.km[t],
+                                              e.cse_schedule, e.cse_sums, self.fac[t],
+                                              e.term_ptr, e.term_elem, omega)
+                    else:
+                        ok.gs_scaling_tensor_3d(n, g.lat.base, uloc, fv, self.km[t],
+                                                self.sh[t], omega)
+                elif self.variant == "nodal":
                     e = self.env
                     ok.gs_nodal_3d(n, g.lat.base, uloc, fv, self.coeff.values[t],
                                    e.cse_schedule, e.cse_sums, self.fac[t], e.term_ptr,

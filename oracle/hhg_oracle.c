@@ -172,6 +172,125 @@ int oracle_gs_nodal_3d(int64_t n, const int64_t *base, double *u, const double *
   return ORACLE_OK;
 }
 
+/* ---- tensor coefficients: km is [M][L], shm [M][14], fac [M][72] ---- */
+
+/* s_d of the scaled tensor row, kernels.py:224-228 */
+static inline double tensor_scaled(const double *km, int64_t M, int64_t L, int64_t p,
+                                   int64_t q, const double *shm, int d) {
+  double s = 0.0;
+  for (int64_t m = 0; m < M; ++m) s += (km[m * L + p] + km[m * L + q]) * shm[m * 14 + d];
+  return s;
+}
+
+/* element sums of every component (kernels.py:268-274); es is [M][24] */
+static void tensor_esums(const double *km, int64_t M, int64_t L, int64_t p,
+                         const int64_t nb[14], const int64_t *sched, int64_t nsched,
+                         const int64_t *sums, double *es) {
+  double buf[55];
+  for (int64_t m = 0; m < M; ++m) {
+    nodal_sums(km + m * L, p, nb, sched, nsched, buf);
+    for (int e = 0; e < 24; ++e) es[m * 24 + e] = buf[sums[e]];
+  }
+}
+
+/* s_d of the nodal tensor row, kernels.py:277-281 (terms outer, m inner) */
+static inline double tensor_nodal(const double *es, int64_t M, const double *fac,
+                                  const int64_t *tptr, const int64_t *telem, int d) {
+  double s = 0.0;
+  for (int64_t t = tptr[d]; t < tptr[d + 1]; ++t)
+    for (int64_t m = 0; m < M; ++m) s += es[m * 24 + telem[t]] * fac[m * 72 + t];
+  return s;
+}
+
+#define ORACLE_MAXM 8
+
+/* kernels.py:192-232 */
+void oracle_apply_scaling_tensor_3d(int64_t n, const int64_t *base, const double *v,
+                                    const double *km, int64_t M, const double *shm,
+                                    double *out) {
+  const int64_t n1 = n + 1, L = (n + 1) * (n + 2) * (n + 3) / 6;
+  int64_t c = 0, nb[14];
+  FOR_VOLUME(n) {
+    const int64_t p = base[k * n1 + j] + i;
+    neighbours(base, n1, k, j, i, nb);
+    const double v0 = v[p];
+    double acc = 0.0;
+    for (int d = 0; d < 14; ++d)
+      acc += tensor_scaled(km, M, L, p, nb[d], shm, d) * (v[nb[d]] - v0);
+    out[c++] = acc;
+  }
+}
+
+/* kernels.py:235-286 */
+int oracle_apply_nodal_tensor_3d(int64_t n, const int64_t *base, const double *v,
+                                 const double *km, int64_t M, const int64_t *sched,
+                                 int64_t nsched, const int64_t *sums, const double *fac,
+                                 const int64_t *tptr, const int64_t *telem, double *out) {
+  if (M > ORACLE_MAXM) return -1;
+  const int64_t n1 = n + 1, L = (n + 1) * (n + 2) * (n + 3) / 6;
+  int64_t c = 0, nb[14];
+  double es[ORACLE_MAXM * 24];
+  FOR_VOLUME(n) {
+    const int64_t p = base[k * n1 + j] + i;
+    neighbours(base, n1, k, j, i, nb);
+    tensor_esums(km, M, L, p, nb, sched, nsched, sums, es);
+    const double v0 = v[p];
+    double acc = 0.0;
+    for (int d = 0; d < 14; ++d)
+      acc += tensor_nodal(es, M, fac, tptr, telem, d) * (v[nb[d]] - v0);
+    out[c++] = acc;
+  }
+  return ORACLE_OK;
+}
+
+/* kernels.py:603-640 */
+int oracle_gs_scaling_tensor_3d(int64_t n, const int64_t *base, double *u, const double *fv,
+                                const double *km, int64_t M, const double *shm,
+                                double omega) {
+  const int64_t n1 = n + 1, L = (n + 1) * (n + 2) * (n + 3) / 6;
+  int64_t c = 0, nb[14];
+  FOR_VOLUME(n) {
+    const int64_t p = base[k * n1 + j] + i;
+    neighbours(base, n1, k, j, i, nb);
+    double acc = 0.0, diag = 0.0;
+    for (int d = 0; d < 14; ++d) {
+      const double s = tensor_scaled(km, M, L, p, nb[d], shm, d);
+      acc += s * u[nb[d]];
+      diag -= s;
+    }
+    if (diag == 0.0) return ORACLE_ZERO_DIAG;
+    u[p] = (1.0 - omega) * u[p] + omega * (fv[c] - acc) / diag;
+    ++c;
+  }
+  return ORACLE_OK;
+}
+
+/* kernels.py:643-702 */
+int oracle_gs_nodal_tensor_3d(int64_t n, const int64_t *base, double *u, const double *fv,
+                              const double *km, int64_t M, const int64_t *sched,
+                              int64_t nsched, const int64_t *sums, const double *fac,
+                              const int64_t *tptr, const int64_t *telem, double omega) {
+  if (M > ORACLE_MAXM) return -1;
+  const int64_t n1 = n + 1, L = (n + 1) * (n + 2) * (n + 3) / 6;
+  int64_t c = 0, nb[14];
+  double es[ORACLE_MAXM * 24];
+  FOR_VOLUME(n) {
+    const int64_t p = base[k * n1 + j] + i;
+    neighbours(base, n1, k, j, i, nb);
+    tensor_esums(km, M, L, p, nb, sched, nsched, sums, es);
+    double acc = 0.0, diag = 0.0;
+    for (int d = 0; d < 14; ++d) {
+      const double s = tensor_nodal(es, M, fac, tptr, telem, d);
+      acc += s * u[nb[d]];
+      diag -= s;
+    }
+    if (diag == 0.0) return ORACLE_ZERO_DIAG;
+    u[p] = (1.0 - omega) * u[p] + omega * (fv[c] - acc) / diag;
+    ++c;
+  }
+  return ORACLE_OK;
+}
+
 /* kernels.py:979-992 */
 int oracle_csr_gs(int64_t nrows, const int64_t *rows, const int32_t *indptr,
                   const int32_t *indices, const double *data, const double *diag,

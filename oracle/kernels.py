@@ -34,6 +34,12 @@ def _load():
         "oracle_csr_gs": (ctypes.c_int, [_I, _P, _P, _P, _P, _P, _P, _P, _D]),
         "oracle_apply_scaling_3d_batch": (None, [_I, _P, _I, _P, _P, _P, _P, _I]),
         "oracle_num_threads": (ctypes.c_int, []),
+        "oracle_apply_scaling_tensor_3d": (None, [_I, _P, _P, _P, _I, _P, _P]),
+        "oracle_apply_nodal_tensor_3d": (ctypes.c_int, [_I, _P, _P, _P, _I, _P, _I, _P, _P,
+                                                        _P, _P, _P]),
+        "oracle_gs_scaling_tensor_3d": (ctypes.c_int, [_I, _P, _P, _P, _P, _I, _P, _D]),
+        "oracle_gs_nodal_tensor_3d": (ctypes.c_int, [_I, _P, _P, _P, _P, _I, _P, _I, _P, _P,
+                                                     _P, _P, _D]),
     }
     for name, (res, args) in sig.items():
         f = getattr(h, name)
@@ -109,6 +115,48 @@ def gs_nodal_3d(n, base, u, fv, kc, sched, sums, fac, tptr, telem, omega):
     rc = lib().oracle_gs_nodal_3d(n, _p(a[0]), _p(u), _p(a[1]), _p(a[2]), _p(a[3]),
                                   len(a[3]), _p(a[4]), _p(a[5]), _p(a[6]), _p(a[7]),
                                   float(omega))
+    if rc:
+        raise ValueError("zero central stencil entry")
+    return u
+
+
+def apply_scaling_tensor_3d(n, base, v, km, shm):
+    """km: (M, L), shm: (M, 14) (kernels.py:192-232)."""
+    out = np.empty(nvol_of(n))
+    base, v, km, shm = _c(base, np.int64), _c(v, float), _c(km, float), _c(shm, float)
+    lib().oracle_apply_scaling_tensor_3d(n, _p(base), _p(v), _p(km), km.shape[0], _p(shm),
+                                         _p(out))
+    return out
+
+
+def apply_nodal_tensor_3d(n, base, v, km, sched, sums, fac, tptr, telem):
+    """km: (M, L), fac: (M, 72) (kernels.py:235-286)."""
+    out = np.empty(nvol_of(n))
+    a = [_c(base, np.int64), _c(v, float), _c(km, float), _c(sched, np.int64),
+         _c(sums, np.int64), _c(fac, float), _c(tptr, np.int64), _c(telem, np.int64)]
+    rc = lib().oracle_apply_nodal_tensor_3d(n, _p(a[0]), _p(a[1]), _p(a[2]), a[2].shape[0],
+                                            _p(a[3]), len(a[3]), _p(a[4]), _p(a[5]),
+                                            _p(a[6]), _p(a[7]), _p(out))
+    if rc:
+        raise ValueError("too many tensor components for the oracle")
+    return out
+
+
+def gs_scaling_tensor_3d(n, base, u, fv, km, shm, omega):
+    base, fv, km, shm = _c(base, np.int64), _c(fv, float), _c(km, float), _c(shm, float)
+    rc = lib().oracle_gs_scaling_tensor_3d(n, _p(base), _p(u), _p(fv), _p(km), km.shape[0],
+                                           _p(shm), float(omega))
+    if rc:
+        raise ValueError("zero central stencil entry")
+    return u
+
+
+def gs_nodal_tensor_3d(n, base, u, fv, km, sched, sums, fac, tptr, telem, omega):
+    a = [_c(base, np.int64), _c(fv, float), _c(km, float), _c(sched, np.int64),
+         _c(sums, np.int64), _c(fac, float), _c(tptr, np.int64), _c(telem, np.int64)]
+    rc = lib().oracle_gs_nodal_tensor_3d(n, _p(a[0]), _p(u), _p(a[1]), _p(a[2]),
+                                         a[2].shape[0], _p(a[3]), len(a[3]), _p(a[4]),
+                                         _p(a[5]), _p(a[6]), _p(a[7]), float(omega))
     if rc:
         raise ValueError("zero central stencil entry")
     return u

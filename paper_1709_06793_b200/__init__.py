@@ -7,7 +7,8 @@ application, residual, smoothing sweep and solver vector update runs in the
 sm_100a kernels of libhhg_b200.so (csrc/), called through its C ABI
 (include/hhg_b200.h).
 """
-from .coefficients import CoefficientField, catalog, kmin_field, sample_nodal
+from .coefficients import (CoefficientField, TensorCoefficient, catalog, kmin_field,
+                           sample_nodal)
 from .costmodel import analytic_count, traffic
 from .mesh import (DIRS_3D, MacroMesh, PrimitiveKind, RefinedGrid,
                    SimplexLattice, cylinder_shell_box, kuhn_blocks,

@@ -87,6 +87,26 @@ EXPORTS = {
                                               vp, vp, vp]),
     "hhg_smooth_volume": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int, vp,
                                          ctypes.c_double, vp, vp, vp]),
+    "hhg_apply_scaling_tensor_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp,
+                                                   ctypes.c_int64, vp, vp, vp]),
+    "hhg_apply_nodal_tensor_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, ctypes.c_int64,
+                                                 c_i64p, ctypes.c_int64, c_i64p, vp, c_i64p,
+                                                 c_i64p, vp, vp]),
+    "hhg_gs_scaling_tensor_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp,
+                                                ctypes.c_int64, vp, ctypes.c_double, vp]),
+    "hhg_gs_nodal_tensor_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int64,
+                                              c_i64p, ctypes.c_int64, c_i64p, vp, c_i64p,
+                                              c_i64p, ctypes.c_double, vp]),
+    "hhg_tensor_volume_apply": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int,
+                                               ctypes.c_int, ctypes.c_int, vp, vp, vp, vp,
+                                               vp, vp]),
+    "hhg_tensor_smooth_volume": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int,
+                                                ctypes.c_int, vp, vp, ctypes.c_double, vp,
+                                                vp, vp]),
+    "hhg_tensor_surface_prepare": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                                  ctypes.POINTER(HhgSurface),
+                                                  ctypes.POINTER(HhgSurfaceGS), ctypes.c_int,
+                                                  vp, vp]),
     "hhg_dot": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),
     "hhg_axpy_ratio": (ctypes.c_int, [ctypes.c_int64, vp, vp, ctypes.c_double, vp,
                                       vp, vp]),

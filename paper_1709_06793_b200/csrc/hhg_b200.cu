@@ -11,6 +11,7 @@
 #include "hhg_common.cuh"
 #include "hhg_smooth.cuh"
 #include "hhg_surface.cuh"
+#include "hhg_tensor.cuh"
 #include "hhg_volume.cuh"
 
 using namespace hhg;
@@ -539,6 +540,168 @@ int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double
   else
     gs_volume_kernel<0><<<g->ntets, gs_volume_threads<0>(), 0, S(stream)>>>(G);
   return check("gs_volume_kernel");
+}
+
+// ---------------------------------------------------------------------------
+// tensor-coefficient operators (M = 6 components, hhg_tensor.cuh)
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+template <bool NODAL>
+static int ten_smem_ok() {
+  static bool done = false;
+  if (!done) {
+    const int smem = (int)ten_smem<NODAL>(ten_threads<NODAL>());
+    if (cudaFuncSetAttribute(tensor_volume_kernel<NODAL, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ||
+        cudaFuncSetAttribute(tensor_volume_kernel<NODAL, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ||
+        cudaFuncSetAttribute(tensor_gs_kernel<NODAL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+      return HHG_ERR_CUDA;
+    done = true;
+  }
+  return HHG_OK;
+}
+
+template <bool NODAL>
+static int ten_apply(const TenDesc &D, bool res, cudaStream_t st) {
+  if (D.n < 4) return HHG_OK;
+  int rc = ten_smem_ok<NODAL>();
+  if (rc) return rc;
+  constexpr int R = ten_rows<NODAL>();
+  const dim3 grid(D.n - 3, (D.n - 3 + R - 1) / R, D.ntets), block(32, R);
+  const size_t smem = ten_smem<NODAL>(ten_threads<NODAL>());
+  if (res) tensor_volume_kernel<NODAL, true><<<grid, block, smem, st>>>(D);
+  else tensor_volume_kernel<NODAL, false><<<grid, block, smem, st>>>(D);
+  return check("tensor_volume_kernel");
+}
+
+template <bool NODAL>
+static int ten_gs(TenDesc D, cudaStream_t st) {
+  if (D.n < 4) return HHG_OK;
+  int rc = ten_smem_ok<NODAL>();
+  if (rc) return rc;
+  rc = hyperplanes(D.n, &D.hp_ptr, &D.hp_code);
+  if (rc) return rc;
+  tensor_gs_kernel<NODAL><<<D.ntets, ten_threads<NODAL>(),
+                            ten_smem<NODAL>(ten_threads<NODAL>()), st>>>(D);
+  return check("tensor_gs_kernel");
+}
+
+static TenDesc ten_elem(int64_t n, const double *v, const double *km, const double *coef) {
+  TenDesc D{};
+  D.n = (int)n;
+  D.ntets = 1;
+  D.L = tetra(n);
+  D.nvol = n >= 4 ? tetra(n - 4) : 0;
+  D.km = km;
+  D.u = v;
+  D.coef = coef;
+  D.lattice = 1;
+  return D;
+}
+
+static TenDesc ten_grid(const hhg_grid *g, const double *km, const double *coef) {
+  TenDesc D{};
+  D.n = g->n;
+  D.ntets = g->ntets;
+  D.L = g->lat_size;
+  D.S = g->shell_size;
+  D.nvol = g->nvol;
+  D.vol_start = reinterpret_cast<const long long *>(g->vol_start);
+  D.ghost = g->ghost;
+  D.km = km;
+  D.coef = coef;
+  D.lattice = 0;
+  return D;
+}
+
+extern "C" {
+
+int hhg_apply_scaling_tensor_3d(int64_t n, const int64_t *, const double *v,
+                                const double *km, int64_t M, const double *shm,
+                                double *out, void *stream) {
+  if (M != kTenM) return HHG_ERR_ARG;
+  TenDesc D = ten_elem(n, v, km, shm);
+  D.out = out;
+  return ten_apply<false>(D, false, S(stream));
+}
+
+int hhg_apply_nodal_tensor_3d(int64_t n, const int64_t *, const double *v, const double *km,
+                              int64_t M, const int64_t *sched, int64_t nsched,
+                              const int64_t *sums, const double *fac, const int64_t *tptr,
+                              const int64_t *telem, double *out, void *stream) {
+  if (M != kTenM) return HHG_ERR_ARG;
+  if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
+  TenDesc D = ten_elem(n, v, km, fac);
+  D.out = out;
+  return ten_apply<true>(D, false, S(stream));
+}
+
+int hhg_gs_scaling_tensor_3d(int64_t n, const int64_t *, double *u, const double *fv,
+                             const double *km, int64_t M, const double *shm, double omega,
+                             void *stream) {
+  if (M != kTenM) return HHG_ERR_ARG;
+  TenDesc D = ten_elem(n, u, km, shm);
+  D.f = fv;
+  D.omega = omega;
+  return ten_gs<false>(D, S(stream));
+}
+
+int hhg_gs_nodal_tensor_3d(int64_t n, const int64_t *, double *u, const double *fv,
+                           const double *km, int64_t M, const int64_t *sched, int64_t nsched,
+                           const int64_t *sums, const double *fac, const int64_t *tptr,
+                           const int64_t *telem, double omega, void *stream) {
+  if (M != kTenM) return HHG_ERR_ARG;
+  if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
+  TenDesc D = ten_elem(n, u, km, fac);
+  D.f = fv;
+  D.omega = omega;
+  return ten_gs<true>(D, S(stream));
+}
+
+int hhg_tensor_volume_apply(const hhg_grid *g, int variant, int flags, int M,
+                            const double *km, const double *coef, const double *u,
+                            const double *f, double *out, void *stream) {
+  if (M != kTenM) return HHG_ERR_ARG;
+  if (variant != HHG_VAR_SCALING && variant != HHG_VAR_NODAL) return HHG_ERR_ARG;
+  TenDesc D = ten_grid(g, km, coef);
+  D.u = u;
+  D.f = f;
+  D.out = out;
+  const bool res = (flags & HHG_FLAG_RESIDUAL) != 0;
+  if (res && !f) return HHG_ERR_ARG;
+  return variant == HHG_VAR_NODAL ? ten_apply<true>(D, res, S(stream))
+                                  : ten_apply<false>(D, res, S(stream));
+}
+
+int hhg_tensor_smooth_volume(const hhg_grid *g, int variant, int M, const double *km,
+                             const double *coef, double omega, double *u, const double *f,
+                             void *stream) {
+  if (M != kTenM) return HHG_ERR_ARG;
+  if (variant != HHG_VAR_SCALING && variant != HHG_VAR_NODAL) return HHG_ERR_ARG;
+  TenDesc D = ten_grid(g, km, coef);
+  D.u = u;
+  D.f = f;
+  D.omega = omega;
+  return variant == HHG_VAR_NODAL ? ten_gs<true>(D, S(stream)) : ten_gs<false>(D, S(stream));
+}
+
+int hhg_tensor_surface_prepare(const hhg_grid *g, const hhg_surface *s,
+                               const hhg_surface_gs *gs, int M, const double *km,
+                               void *stream) {
+  if (M != kTenM) return HHG_ERR_ARG;
+  if (s->nrows <= 0) return HHG_OK;
+  SurfGSDesc G{};
+  G.s = surf_desc(g, s);
+  G.shell_gid = reinterpret_cast<const long long *>(g->shell_gid);
+  G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
+  G.ent_col = gs->ent_col;
+  G.ent_val = gs->ent_val;
+  G.row_diag = gs->row_diag;
+  tensor_surface_fill_kernel<<<(int)((s->nrows + 127) / 128), 128, 0, S(stream)>>>(G, km);
+  return check("tensor_surface_fill_kernel");
 }
 
 int hhg_status(void) {

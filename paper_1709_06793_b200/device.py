@@ -248,7 +248,7 @@ class DeviceGrid:
 
 
 class DeviceSurface:
-    def __init__(self, st: SurfaceTables, psh, pfac):
+    def __init__(self, st: SurfaceTables, psh, pfac, tensor=None):
         torch = require_cuda()
         dev = torch.device("cuda")
         t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
@@ -291,6 +291,7 @@ class DeviceSurface:
         self.ref = ctypes.byref(d)
         self._levels = None
         self._csr = None
+        self.tensor = tensor          # (M, device km [ntets*M*L]) or None
 
     def csr(self, dg):
         """Precomputed surface rows (neighbour ids + weights, filled on the
@@ -307,9 +308,15 @@ class DeviceSurface:
             d = HhgSurfaceGS()
             d.ent_ptr, d.ent_col = keep[0].data_ptr(), keep[1].data_ptr()
             d.ent_val, d.row_diag = keep[2].data_ptr(), keep[3].data_ptr()
-            check(lib.hhg_smooth_surface_prepare(dg.ref, self.ref, ctypes.byref(d),
-                                                 torch.cuda.current_stream().cuda_stream),
-                  "smooth_surface_prepare")
+            stream = torch.cuda.current_stream().cuda_stream
+            if self.tensor is not None:
+                M, km = self.tensor
+                check(lib.hhg_tensor_surface_prepare(dg.ref, self.ref, ctypes.byref(d), M,
+                                                     km.data_ptr(), stream),
+                      "tensor_surface_prepare")
+            else:
+                check(lib.hhg_smooth_surface_prepare(dg.ref, self.ref, ctypes.byref(d),
+                                                     stream), "smooth_surface_prepare")
             self._csr = {"desc": d, "ref": ctypes.byref(d), "keep": keep}
         return self._csr
 

@@ -23,14 +23,15 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, lib
-from .coefficients import CoefficientField
+from .coefficients import CoefficientField, TensorCoefficient
 from .costmodel import analytic_count
 from .device import (DeviceGrid, DeviceSurface, GridTables, SurfaceTables,
                      require_cuda)
 from .mesh import PrimitiveKind
 from .reference_stencils import (classify_edge_types, environment,
                                  nodal_factors, partial_stencils,
-                                 reference_stencil)
+                                 reference_stencil, tensor_component_coeffs,
+                                 tensor_tables)
 
 __all__ = ["Operator", "VARIANTS", "parse_hybrid_set"]
 
@@ -69,7 +70,7 @@ class Operator:
         self.coeff = coeff
         self.hybrid_nodal = frozenset(hybrid_nodal)
         self.dim = grid.dim
-        self.is_tensor = False
+        self.is_tensor = isinstance(coeff, TensorCoefficient)
         self.flops_add = 0
         self.flops_mul = 0
         self.ma2_marked = None
@@ -82,6 +83,14 @@ class Operator:
             self.const_value = 1.0 if coeff is None else float(coeff)
             if self.const_value <= 0:
                 raise ValueError("constant coefficient must be positive")
+        elif self.is_tensor:
+            if variant == "scaling_ma2":
+                raise ValueError("the safeguard is defined for scalar "
+                                 "coefficients only")
+            if coeff.grid is not grid:
+                raise ValueError("coefficient sampled on a different grid")
+            if surface_mode != "csr":
+                raise ValueError("tensor operators use the precomputed surface rows")
         else:
             if not isinstance(coeff, CoefficientField) and not (
                     hasattr(coeff, "values") and hasattr(coeff, "grid")):
@@ -96,9 +105,39 @@ class Operator:
         self._dev = None
 
     # -- host setup (tables only; no operator arithmetic) --------------------
+    def _setup_tensor_tables(self):
+        """Per element and component: half stencils shm (M, 14), nodal
+        factors facm (M, 72) (operators.py:221-238), and the one-sided
+        partial stencils of the surface rows, [element][M][class][...]."""
+        grid = self.grid
+        ne = grid.macro.n_elements
+        self._sh, self._fac = [], []
+        for t in range(ne):
+            shm, facm = tensor_tables(grid, t, self.coeff.dirs)
+            self._sh.append(shm)
+            self._fac.append(facm)
+        cfs = tensor_component_coeffs(self.coeff.dirs, self._env.nshapes)
+        psh = np.zeros((ne, len(cfs), 14, 14))
+        pfac = np.zeros((ne, len(cfs), 14, 72))
+        for t in range(ne):
+            for m, cf in enumerate(cfs):
+                psh[t, m], pfac[t, m] = partial_stencils(grid, t, coeff=cf)
+        self._psh, self._pfac = psh, pfac
+        stack = self._fac if self.variant == "nodal" else self._sh
+        self._coef = np.ascontiguousarray(np.stack(stack)) if ne else np.zeros((0, 6, 14))
+        self._mirror = False
+        if self.variant == "nodal":
+            self._nodal_kinds = frozenset(PrimitiveKind)
+        elif self.variant == "hybrid":
+            self._nodal_kinds = self.hybrid_nodal
+        else:
+            self._nodal_kinds = frozenset()
+
     def _setup_tables(self):
         grid = self.grid
         ne = grid.macro.n_elements
+        if self.is_tensor:
+            return self._setup_tensor_tables()
         self._sh, self._fac = [], []
         if self.variant == "scaling_ma2":
             self._warn_3d_safeguard()
@@ -157,13 +196,18 @@ class Operator:
             torch = require_cuda()
             grid = self.grid
             gt = GridTables(grid)
+            km = None
             if self.variant == "const":
                 kc = np.full((gt.ntets, gt.L), self.const_value)
+            elif self.is_tensor:
+                kc = self.coeff.fields[0].values
+                km = torch.as_tensor(self.coeff.packed(), device="cuda").reshape(-1)
             else:
                 kc = self.coeff.values
             dg = DeviceGrid(gt, kc)
             st = SurfaceTables(grid, gt, self._nodal_kinds)
-            ds = DeviceSurface(st, self._psh, self._pfac)
+            ds = DeviceSurface(st, self._psh, self._pfac,
+                               tensor=(self.coeff.M, km) if self.is_tensor else None)
             coef = torch.as_tensor(self._coef, device="cuda").reshape(-1)
             w = None
             if self._stored is not None:
@@ -176,11 +220,13 @@ class Operator:
                 fac = torch.as_tensor(np.ascontiguousarray(np.stack(self._fac)),
                                       device="cuda").reshape(-1)
             self._dev = {"grid": dg, "surf": ds, "coef": coef, "w": w, "torch": torch,
-                         "sh": sh, "fac": fac}
+                         "sh": sh, "fac": fac, "km": km}
         return self._dev
 
     def _vol_flags(self, residual=False):
         f = _lib.FLAG_RESIDUAL if residual else 0
+        if self.is_tensor and self._stored is None:
+            return f
         if self.fast and self.variant != "nodal":
             f |= _lib.FLAG_FAST
         elif self._mirror and self._vol_variant() == _lib.VAR["scaling"]:
@@ -241,9 +287,15 @@ class Operator:
         fp = f.data_ptr() if f is not None else None
         check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
         wp = D["w"].data_ptr() if D["w"] is not None else None
-        check(lib.hhg_volume_apply(dg.ref, self._vol_variant(), flags,
-                                   D["coef"].data_ptr(), wp, du.data_ptr(), fp,
-                                   out.data_ptr(), st), "volume_apply")
+        if self.is_tensor and self._stored is None:
+            check(lib.hhg_tensor_volume_apply(dg.ref, self._vol_variant(), flags,
+                                              self.coeff.M, D["km"].data_ptr(),
+                                              D["coef"].data_ptr(), du.data_ptr(), fp,
+                                              out.data_ptr(), st), "tensor_volume_apply")
+        else:
+            check(lib.hhg_volume_apply(dg.ref, self._vol_variant(), flags,
+                                       D["coef"].data_ptr(), wp, du.data_ptr(), fp,
+                                       out.data_ptr(), st), "volume_apply")
         self._surface(dg, ds, flags & _lib.FLAG_RESIDUAL, du, fp, out, st)
         self._count()
         return out
@@ -354,7 +406,7 @@ class Operator:
     # -- public operations (reference signatures) ------------------------------
     def apply(self, u):
         """Matrix action A u with identity on Dirichlet rows."""
-        du, kind = self._to_dev(u, pipelined=True)
+        du, kind = self._to_dev(u, pipelined=not self.is_tensor)
         if kind == "host-pipe":
             return self.apply_host(du)
         return self._from_dev(self.apply_device(du), kind)
@@ -376,6 +428,26 @@ class Operator:
         st = self._stream()
         gs = ds.gs_tables(dg)
         src = getattr(self, "source_variant", self.variant)
+        if self.is_tensor:
+            var = _lib.VAR["nodal"] if src == "nodal" else _lib.VAR["scaling"]
+            coef = D.get("tcoef")
+            if coef is None:
+                stack = self._fac if src == "nodal" else self._sh
+                coef = D["tcoef"] = D["torch"].as_tensor(
+                    np.ascontiguousarray(np.stack(stack)), device="cuda").reshape(-1)
+            lib.hhg_status_reset()
+            for _ in range(sweeps):
+                check(lib.hhg_smooth_surface_all(dg.ref, ds.ref, gs["ref"], float(omega),
+                                                 du.data_ptr(), df.data_ptr(), st),
+                      "smooth_surface")
+                check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
+                check(lib.hhg_tensor_smooth_volume(dg.ref, var, self.coeff.M,
+                                                   D["km"].data_ptr(), coef.data_ptr(),
+                                                   float(omega), du.data_ptr(),
+                                                   df.data_ptr(), st), "tensor_smooth_volume")
+            D["torch"].cuda.current_stream().synchronize()
+            check(lib.hhg_status(), "smooth")
+            return du
         if src == "nodal":
             var, coef = _lib.VAR["nodal"], D["coef"] if self._stored is None else D["fac"]
         else:
@@ -405,6 +477,8 @@ class Operator:
 
     def _count(self, napplies=1):
         v = self.variant
+        if self.is_tensor:
+            return
         if v in ("scaling", "scaling_ma2", "hybrid"):
             cnt = analytic_count("scaling", 3)
         elif v in ("nodal", "const", "stored"):
@@ -434,6 +508,8 @@ class Operator:
             w[:, 0] = -s.sum()
             w[:, 1:] = s
             return w
+        if self.is_tensor:
+            return self._tensor_weights(t, p, nb, w)
         kv = self.coeff.values[t]
         k0 = kv[p]
         if self.variant == "nodal":
@@ -461,6 +537,43 @@ class Operator:
             sd = (k0 + kv[nb[d]]) * sh[d]
             w[:, 1 + d] = sd
             tot = tot + sd
+        w[:, 0] = -tot
+        return w
+
+    def _tensor_weights(self, t, p, nb, w):
+        """Tensor stencil table (dump_scaling_tensor_3d / dump_nodal_tensor_3d,
+        kernels.py:377-468), same association order."""
+        km = [f.values[t] for f in self.coeff.fields]
+        M = len(km)
+        tot = np.zeros(len(p))
+        if self.variant == "nodal":
+            env = self._env
+            fac = self._fac[t]
+            es = []
+            for m in range(M):
+                buf = np.empty((len(p), 55))
+                buf[:, 0] = km[m][p]
+                for d in range(14):
+                    buf[:, 1 + d] = km[m][nb[d]]
+                for dst, a, b in env.cse_schedule:
+                    buf[:, dst] = buf[:, a] + buf[:, b]
+                es.append(buf[:, env.cse_sums])
+            for d in range(14):
+                s = np.zeros(len(p))
+                for tt in range(env.term_ptr[d], env.term_ptr[d + 1]):
+                    e = env.term_elem[tt]
+                    for m in range(M):
+                        s = s + es[m][:, e] * fac[m, tt]
+                w[:, 1 + d] = s
+                tot = tot + s
+        else:
+            shm = self._sh[t]
+            for d in range(14):
+                s = np.zeros(len(p))
+                for m in range(M):
+                    s = s + (km[m][p] + km[m][nb[d]]) * shm[m, d]
+                w[:, 1 + d] = s
+                tot = tot + s
         w[:, 0] = -tot
         return w
 

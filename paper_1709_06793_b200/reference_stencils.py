@@ -145,27 +145,33 @@ def element_gradients(verts):
 
 
 def element_stiffness(verts, coeff=None):
-    """Exact P1 stiffness matrices vol * grad_i . grad_j (optionally with a
-    per-element scalar coefficient)."""
+    """Exact P1 stiffness matrices vol * grad_i . K grad_j; coeff is None,
+    per-element scalars (m,) or tensors (m, 3, 3)
+    (reference_stencils.py:196-215)."""
     grads, vol = element_gradients(verts)
     single = grads.ndim == 2
     if single:
         grads, vol = grads[None], np.atleast_1d(vol)
     if coeff is None:
         A = np.einsum("mid,mjd->mij", grads, grads)
-    else:
+    elif np.ndim(coeff) <= 1:
         A = np.einsum("m,mid,mjd->mij", np.atleast_1d(np.asarray(coeff, float)),
                       grads, grads)
+    else:
+        A = np.einsum("mid,mde,mje->mij", grads, np.asarray(coeff, float), grads)
     A *= vol[:, None, None]
     return A[0] if single else A
 
 
-def environment_matrices(E, level):
+def environment_matrices(E, level, coeff=None):
     """Stiffness matrices of the 24 patch elements of a macro element with
-    edge matrix E at ``level`` (one matrix per shape, expanded by index)."""
+    edge matrix E at ``level`` (one matrix per shape, expanded by index);
+    ``coeff`` is an optional per-shape tensor stack (reference_stencils.py:
+    244-261)."""
     env = environment(3)
     n = 1 << level
-    shape_mats = element_stiffness((env.shape_offsets @ E) / n)
+    verts = (env.shape_offsets @ E) / n
+    shape_mats = element_stiffness(verts) if coeff is None else element_stiffness(verts, coeff)
     p = env.elem_perm
     return env, shape_mats[env.elem_shape[:, None, None], p[:, :, None], p[:, None, :]]
 
@@ -259,14 +265,45 @@ def class_element_masks():
     return inside, dir_inside
 
 
-def partial_stencils(grid, t: int):
+def tensor_component_coeffs(dirs, nshapes):
+    """Per-shape tensor of component m: None for the gradient component,
+    c_m c_m^T otherwise (operators.py:221-230)."""
+    out = []
+    for m, c in enumerate(dirs):
+        if m == 0:
+            out.append(None)
+        else:
+            c = np.asarray(c)
+            out.append(np.broadcast_to(np.outer(c, c), (nshapes, 3, 3)))
+    return out
+
+
+def tensor_tables(grid, t: int, dirs):
+    """(shm (M, 14), facm (M, 72)) of macro element t for the M-component
+    tensor operators: half stencils and nodal factors per component
+    (operators.py:221-238)."""
+    env = environment(3)
+    E = _edge_matrix(grid, t)
+    shm, facm = [], []
+    for cf in tensor_component_coeffs(dirs, env.nshapes):
+        _, mats = environment_matrices(E, grid.level, coeff=cf)
+        s = np.empty(14)
+        for d in range(14):
+            lo, hi = env.term_ptr[d], env.term_ptr[d + 1]
+            s[d] = mats[env.term_elem[lo:hi], 0, env.term_slot[lo:hi]].sum()
+        shm.append(s / 2.0)
+        facm.append(mats[env.term_elem, 0, env.term_slot] / 4)
+    return np.ascontiguousarray(shm), np.ascontiguousarray(facm)
+
+
+def partial_stencils(grid, t: int, coeff=None):
     """Half stencils restricted to the part of the patch inside macro element
     t, for each of the 14 boundary classes: psh[c, d] = 1/2 sum over inside
     elements of A_e[0, slot], and the nodal factors pfac[c, term] (zero for
     outside elements).  A surface row is the sum over the incident macro
     elements of these one-sided rows — the element-wise assembly of
     operators.py:329-365 grouped by neighbour direction."""
-    env, mats = environment_matrices(_edge_matrix(grid, t), grid.level)
+    env, mats = environment_matrices(_edge_matrix(grid, t), grid.level, coeff=coeff)
     inside, _ = class_element_masks()
     vals = mats[env.term_elem, 0, env.term_slot]          # (72,)
     psh = np.zeros((14, 14))

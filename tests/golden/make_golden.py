@@ -273,8 +273,88 @@ def sec_c4_mg():
          u_norm=np.linalg.norm(u))
 
 
+def sec_tensor():
+    """Tensor-coefficient (M = 6) pins: the reference's tensor numba kernels
+    on seeded lattices, tensor Operators (tensor3d_poly on the unit cube,
+    cylinder_blend on the half-cylinder shell box) and a tensor V-cycle."""
+    from hhgscale.coefficients import TensorCoefficient, catalog
+    rng = np.random.default_rng(77)
+    env = r_env(3)
+    out = {}
+    for n in (8, 16):
+        lat = RM.SimplexLattice(3, n)
+        nv = (n - 1) * (n - 2) * (n - 3) // 6
+        v = rng.uniform(-1, 1, lat.size)
+        km = np.ascontiguousarray(rng.uniform(0.2, 2.0, (6, lat.size)))
+        shm = np.ascontiguousarray(rng.uniform(-0.3, 0.1, (6, 14)))
+        fac = np.ascontiguousarray(rng.uniform(-0.2, 0.2, (6, 72)))
+        fv = rng.uniform(-1, 1, nv)
+        o = {"v": v, "km": km, "shm": shm, "fac": fac, "fv": fv}
+        r = np.empty(nv); kn.apply_scaling_tensor_3d(n, lat.base, v, km, shm, r)
+        o["scaling"] = r
+        r = np.empty(nv)
+        kn.apply_nodal_tensor_3d(n, lat.base, v, km, env.cse_schedule, env.cse_sums, fac,
+                                 env.term_ptr, env.term_elem, r)
+        o["nodal"] = r
+        shg = np.ascontiguousarray(-np.abs(shm) - 0.05)
+        facg = np.ascontiguousarray(-np.abs(fac) - 0.01)
+        u = v.copy(); kn.gs_scaling_tensor_3d(n, lat.base, u, fv, km, shg, 1.0)
+        o["gs_scaling"], o["shg"] = u, shg
+        u = v.copy()
+        kn.gs_nodal_tensor_3d(n, lat.base, u, fv, km, env.cse_schedule, env.cse_sums, facg,
+                              env.term_ptr, env.term_elem, 0.9)
+        o["gs_nodal_w09"], o["facg"] = u, facg
+        for key, val in o.items():
+            out[f"n{n}_{key}"] = val
+    save("tensor_kernels", **out)
+
+    def op_set(tag, mesh, level, Kfn, seed, variants, extra):
+        g = RM.RefinedGrid(rmesh(mesh), level)
+        K = TensorCoefficient(g, Kfn)
+        r = np.random.default_rng(seed)
+        u = r.uniform(-1, 1, g.n_nodes)
+        f = r.uniform(-1, 1, g.n_nodes)
+        res = {"u": u, "f": f}
+        for v in variants:
+            hn = frozenset()
+            name = v
+            if v.startswith("hybrid:"):
+                hn = parse_hybrid_set(v.split(":", 1)[1])
+                v = "hybrid"
+            res[f"apply_{name}"] = ROperator(g, v, K, hybrid_nodal=hn).apply(u)
+        if extra:
+            for var in ("scaling", "nodal"):
+                op = ROperator(g, var, K)
+                res[f"residual_{var}"] = op.residual(u, f)
+                res[f"stored_{var}"] = op.store_stencils().apply(u)
+                res[f"weights_{var}_t1"] = op.stencil_weights(1)
+                uu = u.copy()
+                op.smooth(uu, f, sweeps=1, omega=1.0)
+                res[f"smooth_{var}_w1"] = uu
+                uu = u.copy()
+                op.smooth(uu, f, sweeps=2, omega=0.8)
+                res[f"smooth_{var}_2sw_w08"] = uu
+        save(tag, **res)
+
+    op_set("tensor_cube6_l3", M.unit_cube_6(), 3, catalog("tensor3d_poly"), 31,
+           ["scaling", "nodal", "hybrid:wv+we"], True)
+    op_set("tensor_cube6_l5", M.unit_cube_6(), 5, catalog("tensor3d_poly"), 32,
+           ["scaling", "nodal"], False)
+    _, K_cyl = catalog("cylinder_blend")
+    op_set("tensor_cyl_l3", M.cylinder_shell_box(nr=1, na=2, nz=2), 3, K_cyl, 33,
+           ["scaling", "nodal"], True)
+    # tensor V(2,2) cycles (GridHierarchy(..., tensor=True), multigrid.py:117-119)
+    hier = GridHierarchy(RM.unit_cube_6(), 4, "scaling", catalog("tensor3d_poly"), tensor=True)
+    g = hier.grids[4]
+    f = np.random.default_rng(34).normal(size=g.n_nodes)
+    f[g.dirichlet_mask] = 0.0
+    u, rep = solve(hier, f, stop="iters:6", pre=2, post=2)
+    save("tensor_mg", f=f, residuals=np.array(rep.residuals), u=u)
+
+
 SECTIONS = {"mesh": sec_mesh, "kernels": sec_kernels, "applies": sec_applies,
-            "c3": sec_c3_checksums, "c2": sec_c2_cg, "mg": sec_mg_small, "c4": sec_c4_mg}
+            "c3": sec_c3_checksums, "c2": sec_c2_cg, "mg": sec_mg_small, "c4": sec_c4_mg,
+            "tensor": sec_tensor}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(SECTIONS)):
