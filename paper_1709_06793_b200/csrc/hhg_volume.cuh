@@ -697,13 +697,18 @@ volume_kernel_mirror(VolDesc D) {
     for (int m = 0; m < NSLOT; ++m) {
       IncSlot &S = sl_[m];
       const int si = S.ij & 0xffff, sj = S.ij >> 16;
-      if (p <= S.pmax) {
+      {
+        // predicated copies instead of a divergent branch per slot
+        const int live = p <= S.pmax;
         const bool interior = p >= 1 && si >= 1 && sj >= 1 && p < S.pmax;
         const double *vs = interior ? at(T.v, S.vo) : at(T.g, S.go);
         const double *ks = at(T.k, S.ko);
         const unsigned d = off + (unsigned)(threadIdx.x + m * NT) * sizeof(double2);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(vs));
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d + 8), "l"(ks));
+        asm volatile(
+            "{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n"
+            " @q cp.async.ca.shared.global [%0], [%1], 8;\n"
+            " @q cp.async.ca.shared.global [%2], [%3], 8;\n}\n" ::"r"(d),
+            "l"(vs), "r"(d + 8), "l"(ks), "r"(live));
       }
       // advance to plane p + 1
       S.ko += (n - p + 1) * (n - p) / 2 + (n - p + 1) - sj;   // T2(n - p) - j
