@@ -68,6 +68,25 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar) {
 __device__ __forceinline__ void mbar_arrive_cp_async(unsigned bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
+#ifndef HHG_MBAR_PROBE
+#define HHG_MBAR_PROBE 0
+#endif
+#ifndef HHG_LATE_REFILL
+#define HHG_LATE_REFILL 0
+#endif
+// non-blocking probe: the result is consumed a step later, so the
+// ~150-cycle phase check overlaps the arithmetic instead of stalling
+__device__ __forceinline__ unsigned mbar_test(unsigned bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(bar), "r"(parity)
+      : "memory");
+  return ok;
+}
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -689,9 +708,9 @@ volume_kernel_mirror(VolDesc D) {
     sl_[m].go = sl_[m].ko;                                               // plane 0
   }
   const int t2n = (n + 1) * (n + 2) / 2;
-  auto produce = [&](int p) {
+  auto produce = [&](int p, unsigned empty_ok) {
     const int sl = p % NS;
-    if (p >= NS) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
+    if (p >= NS && !empty_ok) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
     const unsigned off = ring_s + (unsigned)sl * PLANE_BYTES;
 #pragma unroll
     for (int m = 0; m < NSLOT; ++m) {
@@ -721,7 +740,7 @@ volume_kernel_mirror(VolDesc D) {
     mbar_arrive_cp_async(full0 + 8 * sl);
   };
 
-  for (int p = 0; p < PD && p <= kmax + 1; ++p) produce(p);
+  for (int p = 0; p < PD && p <= kmax + 1; ++p) produce(p, 0u);
 
   const int li = lane & 7, lj = lane >> 3;
   const int r0 = 1 + lj * B;
@@ -740,14 +759,27 @@ volume_kernel_mirror(VolDesc D) {
   Win<B> X0, X1, X2;
   MirrorCarry<B> carry;
 
-  // fetch plane q into window w and release its slot
+  // fetch plane q into window w and release its slot; then probe (without
+  // blocking) the barriers the next step and this step's producer need
+  unsigned full_ok = 0u, empty_ok = 0u;
   auto fetch = [&](int q, Win<B> &w) {
     const int sl = q % NS;
-    mbar_wait(full0 + 8 * sl, (q / NS) & 1);
+    if (!full_ok) mbar_wait(full0 + 8 * sl, (q / NS) & 1);
     load_win<B>(w, ring + sl * ROWS * VOL_COLS, r0, c);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sl);
-    if (q + PD <= kmax + 1) produce(q + PD);
+#if HHG_MBAR_PROBE
+    const int q1 = q + 1;
+    full_ok = q1 <= kmax + 1 ? mbar_test(full0 + 8 * (q1 % NS), (q1 / NS) & 1) : 1u;
+#endif
+#if HHG_LATE_REFILL == 0
+    if (q + PD <= kmax + 1) produce(q + PD, 0u);
+#endif
+  };
+  auto refill = [&](int q) {
+#if HHG_LATE_REFILL
+    if (q + PD <= kmax + 1) produce(q + PD, empty_ok);
+#endif
   };
   auto emit = [&](int kk, const double (&vals)[B]) {
     const int lim = n - 1 - kk;
@@ -770,11 +802,14 @@ volume_kernel_mirror(VolDesc D) {
       mirror_step<B>(mi, hi, sh, carry, vals);
       emit(q - 1, vals);
     }
+    refill(q);
   };
 
   if (kmax >= 1) {
     fetch(0, X0);
+    refill(0);
     fetch(1, X1);
+    refill(1);
     if (warp_min_ij <= n - 2) mirror_seed<B>(X0, X1, sh, carry);
     step(2, X1, X2);
     for (int q = 3; q <= kmax + 1; q += 3) {

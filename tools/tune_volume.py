@@ -23,8 +23,12 @@ from paper_1709_06793_b200.shard import slab_mesh  # noqa: E402
 from tests.cases import k_c5  # noqa: E402
 
 level = int(os.environ.get("LEVEL", "8"))
-configs = [tuple(int(x) for x in (c + ",2,0,0").split(",")[:5]) for c in
-           os.environ.get("CONFIGS", "2,8,6 1,8,6 2,4,6 3,4,6 1,16,6 2,8,4 2,8,8").split()]
+# CONFIGS items: "B,W,NS[,MINB[,EXPT]][:DEF=1+DEF2=0]" (extra -D macros)
+configs = []
+for c in os.environ.get("CONFIGS", "2,8,6 1,8,6 2,4,6 3,4,6 1,16,6 2,8,4 2,8,8").split():
+    nums, _, extra = c.partition(":")
+    configs.append(tuple(int(x) for x in (nums + ",2,0,0").split(",")[:5]) +
+                   (tuple(e for e in extra.split("+") if e),))
 grid = RefinedGrid(slab_mesh(0, 1), level)
 kf = sample_nodal(k_c5(), grid)
 u = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, grid.n_nodes), device="cuda")
@@ -33,11 +37,11 @@ sh = torch.as_tensor(np.stack([reference_stencil(grid, t)[1] / 2 for t in range(
                      device="cuda").reshape(-1)
 nvol = grid.nodes_per_volume * grid.macro.n_elements
 ref = None
-for B, W, NS, MINB, EXPT in configs:
-    so = f"/tmp/hhg_tune_{B}_{W}_{NS}_{MINB}_{EXPT}.so"
+for B, W, NS, MINB, EXPT, EXTRA in configs:
+    so = f"/tmp/hhg_tune_{B}_{W}_{NS}_{MINB}_{EXPT}_{'_'.join(EXTRA)}.so"
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-DHHG_SCALING_ONLY",
-           f"-DHHG_VOL_B={B}", f"-DHHG_VOL_W={W}", f"-DHHG_VOL_NS={NS}", f"-DHHG_VOL_MINB={MINB}", f"-DHHG_MIRROR_MINB={MINB}", f"-DHHG_VOL_EXPT={EXPT}", "-Xptxas", "-v",
+           f"-DHHG_VOL_B={B}", f"-DHHG_VOL_W={W}", f"-DHHG_VOL_NS={NS}", f"-DHHG_VOL_MINB={MINB}", f"-DHHG_MIRROR_MINB={MINB}", f"-DHHG_VOL_EXPT={EXPT}", *[f"-D{e}" for e in EXTRA], "-Xptxas", "-v",
            "-o", so, str(ROOT / "paper_1709_06793_b200/csrc/hhg_b200.cu")]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode:
@@ -64,6 +68,6 @@ for B, W, NS, MINB, EXPT in configs:
         ms = e0.elapsed_time(e1) / 20
         chk = float(out[grid.n_surface_nodes:].abs().sum())
         if ref is None and EXPT == 0: ref = chk
-        print(f"B={B} W={W} NS={NS} MINB={MINB} EXPT={EXPT} flags={fast} {ms:.3f} ms {nvol/ms/1e6:.1f} GDoF/s "
+        print(f"B={B} W={W} NS={NS} MINB={MINB} EXPT={EXPT} {'+'.join(EXTRA)} flags={fast} {ms:.3f} ms {nvol/ms/1e6:.1f} GDoF/s "
               f"regs={regs[0].split('Used')[1].split(',')[0].strip() if regs else '?'} chk_ok={ref is not None and abs(chk-ref)<=1e-9*ref}", flush=True)
     del dg
