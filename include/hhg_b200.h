@@ -258,15 +258,20 @@ int hhg_gs_nodal_tensor_3d(int64_t n, const int64_t *base, double *u,
 
 /* batched volume rows of the tensor operators (Operator._run_volume tensor
  * branch, operators.py:406-426): variant HHG_VAR_SCALING or HHG_VAR_NODAL;
- * km [ntets][M][L], coef [ntets][M][14 | 72]; flags: HHG_FLAG_RESIDUAL */
+ * km [ntets][L][M] (all components of a point contiguous), coef
+ * [ntets][M][14 | 72]; flags: HHG_FLAG_RESIDUAL.  work: caller-owned
+ * float64[ntets * lat_size] scratch: u is gathered into element lattices
+ * first (the reference's u[elem_gidx[t]], operators.py:383; ghost shells
+ * must be current), the smoother scatters the interior back afterwards. */
 int hhg_tensor_volume_apply(const hhg_grid *g, int variant, int flags, int M,
                             const double *km, const double *coef, const double *u,
-                            const double *f, double *out, void *stream);
+                            const double *f, double *out, double *work, void *stream);
 int hhg_tensor_smooth_volume(const hhg_grid *g, int variant, int M, const double *km,
                              const double *coef, double omega, double *u,
-                             const double *f, void *stream);
+                             const double *f, double *work, void *stream);
 /* surface rows of the tensor operators (operators.py:277-327 tensor branch):
- * s->psh is [ntets][M][14][14], s->pfac [ntets][M][14][72]; fills the same
+ * s->psh is [ntets][M][14][14], s->pfac [ntets][M][14][72], km as above
+ * ([ntets][L][M]); fills the same
  * precomputed rows hhg_smooth_surface_prepare fills for scalar k, so
  * hhg_surface_apply_csr / hhg_smooth_surface_all serve both */
 int hhg_tensor_surface_prepare(const hhg_grid *g, const hhg_surface *s,

@@ -99,10 +99,10 @@ EXPORTS = {
                                               c_i64p, ctypes.c_double, vp]),
     "hhg_tensor_volume_apply": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int,
                                                ctypes.c_int, ctypes.c_int, vp, vp, vp, vp,
-                                               vp, vp]),
+                                               vp, vp, vp]),
     "hhg_tensor_smooth_volume": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int,
                                                 ctypes.c_int, vp, vp, ctypes.c_double, vp,
-                                                vp, vp]),
+                                                vp, vp, vp]),
     "hhg_tensor_surface_prepare": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
                                                   ctypes.POINTER(HhgSurface),
                                                   ctypes.POINTER(HhgSurfaceGS), ctypes.c_int,

@@ -547,16 +547,16 @@ int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double
 // ---------------------------------------------------------------------------
 }  // extern "C"
 
-template <bool NODAL>
+template <bool NODAL, bool AOS>
 static int ten_smem_ok() {
   static bool done = false;
   if (!done) {
     const int smem = (int)ten_smem<NODAL>(ten_threads<NODAL>());
-    if (cudaFuncSetAttribute(tensor_volume_kernel<NODAL, false>,
+    if (cudaFuncSetAttribute(tensor_volume_kernel<NODAL, false, AOS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ||
-        cudaFuncSetAttribute(tensor_volume_kernel<NODAL, true>,
+        cudaFuncSetAttribute(tensor_volume_kernel<NODAL, true, AOS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ||
-        cudaFuncSetAttribute(tensor_gs_kernel<NODAL>,
+        cudaFuncSetAttribute(tensor_gs_kernel<NODAL, AOS>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
       return HHG_ERR_CUDA;
     done = true;
@@ -564,28 +564,28 @@ static int ten_smem_ok() {
   return HHG_OK;
 }
 
-template <bool NODAL>
+template <bool NODAL, bool AOS>
 static int ten_apply(const TenDesc &D, bool res, cudaStream_t st) {
   if (D.n < 4) return HHG_OK;
-  int rc = ten_smem_ok<NODAL>();
+  int rc = ten_smem_ok<NODAL, AOS>();
   if (rc) return rc;
   constexpr int R = ten_rows<NODAL>();
   const dim3 grid(D.n - 3, (D.n - 3 + R - 1) / R, D.ntets), block(32, R);
   const size_t smem = ten_smem<NODAL>(ten_threads<NODAL>());
-  if (res) tensor_volume_kernel<NODAL, true><<<grid, block, smem, st>>>(D);
-  else tensor_volume_kernel<NODAL, false><<<grid, block, smem, st>>>(D);
+  if (res) tensor_volume_kernel<NODAL, true, AOS><<<grid, block, smem, st>>>(D);
+  else tensor_volume_kernel<NODAL, false, AOS><<<grid, block, smem, st>>>(D);
   return check("tensor_volume_kernel");
 }
 
-template <bool NODAL>
+template <bool NODAL, bool AOS>
 static int ten_gs(TenDesc D, cudaStream_t st) {
   if (D.n < 4) return HHG_OK;
-  int rc = ten_smem_ok<NODAL>();
+  int rc = ten_smem_ok<NODAL, AOS>();
   if (rc) return rc;
   rc = hyperplanes(D.n, &D.hp_ptr, &D.hp_code);
   if (rc) return rc;
-  tensor_gs_kernel<NODAL><<<D.ntets, ten_threads<NODAL>(),
-                            ten_smem<NODAL>(ten_threads<NODAL>()), st>>>(D);
+  tensor_gs_kernel<NODAL, AOS><<<D.ntets, ten_threads<NODAL>(),
+                                 ten_smem<NODAL>(ten_threads<NODAL>()), st>>>(D);
   return check("tensor_gs_kernel");
 }
 
@@ -598,7 +598,7 @@ static TenDesc ten_elem(int64_t n, const double *v, const double *km, const doub
   D.km = km;
   D.u = v;
   D.coef = coef;
-  D.lattice = 1;
+  D.out_split = 0;
   return D;
 }
 
@@ -613,8 +613,17 @@ static TenDesc ten_grid(const hhg_grid *g, const double *km, const double *coef)
   D.ghost = g->ghost;
   D.km = km;
   D.coef = coef;
-  D.lattice = 0;
+  D.out_split = 1;
   return D;
+}
+
+// u (split global layout + current ghost shells) -> element lattices
+static int ten_gather(const TenDesc &G, const double *u, double *lat, cudaStream_t st) {
+  TenDesc D = G;
+  D.u = u;
+  const dim3 grid(D.n + 1, (D.n + 1 + 3) / 4, D.ntets), block(32, 4);
+  lattice_gather_kernel<<<grid, block, 0, st>>>(D, lat);
+  return check("lattice_gather_kernel");
 }
 
 extern "C" {
@@ -625,7 +634,7 @@ int hhg_apply_scaling_tensor_3d(int64_t n, const int64_t *, const double *v,
   if (M != kTenM) return HHG_ERR_ARG;
   TenDesc D = ten_elem(n, v, km, shm);
   D.out = out;
-  return ten_apply<false>(D, false, S(stream));
+  return ten_apply<false, false>(D, false, S(stream));
 }
 
 int hhg_apply_nodal_tensor_3d(int64_t n, const int64_t *, const double *v, const double *km,
@@ -636,7 +645,7 @@ int hhg_apply_nodal_tensor_3d(int64_t n, const int64_t *, const double *v, const
   if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
   TenDesc D = ten_elem(n, v, km, fac);
   D.out = out;
-  return ten_apply<true>(D, false, S(stream));
+  return ten_apply<true, false>(D, false, S(stream));
 }
 
 int hhg_gs_scaling_tensor_3d(int64_t n, const int64_t *, double *u, const double *fv,
@@ -646,7 +655,7 @@ int hhg_gs_scaling_tensor_3d(int64_t n, const int64_t *, double *u, const double
   TenDesc D = ten_elem(n, u, km, shm);
   D.f = fv;
   D.omega = omega;
-  return ten_gs<false>(D, S(stream));
+  return ten_gs<false, false>(D, S(stream));
 }
 
 int hhg_gs_nodal_tensor_3d(int64_t n, const int64_t *, double *u, const double *fv,
@@ -658,34 +667,45 @@ int hhg_gs_nodal_tensor_3d(int64_t n, const int64_t *, double *u, const double *
   TenDesc D = ten_elem(n, u, km, fac);
   D.f = fv;
   D.omega = omega;
-  return ten_gs<true>(D, S(stream));
+  return ten_gs<true, false>(D, S(stream));
 }
 
 int hhg_tensor_volume_apply(const hhg_grid *g, int variant, int flags, int M,
                             const double *km, const double *coef, const double *u,
-                            const double *f, double *out, void *stream) {
-  if (M != kTenM) return HHG_ERR_ARG;
+                            const double *f, double *out, double *work, void *stream) {
+  if (M != kTenM || !work) return HHG_ERR_ARG;
   if (variant != HHG_VAR_SCALING && variant != HHG_VAR_NODAL) return HHG_ERR_ARG;
-  TenDesc D = ten_grid(g, km, coef);
-  D.u = u;
-  D.f = f;
-  D.out = out;
   const bool res = (flags & HHG_FLAG_RESIDUAL) != 0;
   if (res && !f) return HHG_ERR_ARG;
-  return variant == HHG_VAR_NODAL ? ten_apply<true>(D, res, S(stream))
-                                  : ten_apply<false>(D, res, S(stream));
+  if (g->n < 4) return HHG_OK;
+  TenDesc D = ten_grid(g, km, coef);
+  int rc = ten_gather(D, u, work, S(stream));
+  if (rc) return rc;
+  D.u = work;
+  D.f = f;
+  D.out = out;
+  return variant == HHG_VAR_NODAL ? ten_apply<true, true>(D, res, S(stream))
+                                  : ten_apply<false, true>(D, res, S(stream));
 }
 
 int hhg_tensor_smooth_volume(const hhg_grid *g, int variant, int M, const double *km,
                              const double *coef, double omega, double *u, const double *f,
-                             void *stream) {
-  if (M != kTenM) return HHG_ERR_ARG;
+                             double *work, void *stream) {
+  if (M != kTenM || !work) return HHG_ERR_ARG;
   if (variant != HHG_VAR_SCALING && variant != HHG_VAR_NODAL) return HHG_ERR_ARG;
+  if (g->n < 4) return HHG_OK;
   TenDesc D = ten_grid(g, km, coef);
-  D.u = u;
+  int rc = ten_gather(D, u, work, S(stream));
+  if (rc) return rc;
+  D.u = work;
   D.f = f;
   D.omega = omega;
-  return variant == HHG_VAR_NODAL ? ten_gs<true>(D, S(stream)) : ten_gs<false>(D, S(stream));
+  rc = variant == HHG_VAR_NODAL ? ten_gs<true, true>(D, S(stream))
+                                : ten_gs<false, true>(D, S(stream));
+  if (rc) return rc;
+  const dim3 grid(D.n - 3, (D.n - 3 + 3) / 4, D.ntets), block(32, 4);
+  lattice_scatter_kernel<<<grid, block, 0, S(stream)>>>(D, work, u);
+  return check("lattice_scatter_kernel");
 }
 
 int hhg_tensor_surface_prepare(const hhg_grid *g, const hhg_surface *s,

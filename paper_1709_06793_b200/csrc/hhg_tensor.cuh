@@ -28,14 +28,14 @@ constexpr int kTenM = 6;   // 3-D splitting (TENSOR_DIRS_3D)
 struct TenDesc {
   int n, ntets;
   long long L, S, nvol;
-  const long long *vol_start;  // SPLIT: first volume id per element
-  const double *ghost;         // SPLIT: compact shells [ntets*S]
-  const double *km;            // [ntets][M][L]
-  const double *u;             // SPLIT: global vector; LATTICE: [ntets*L]
+  const long long *vol_start;  // first volume id per element (split layout)
+  const double *km;            // [ntets][L][M] (batched) or [M][L] (per element)
+  const double *u;             // element lattices [ntets*L]
+  const double *ghost;         // gather: compact shells [ntets*S]
   const double *f;             // residual / GS rhs (global or [ntets*nvol])
   double *out;                 // apply: global or [ntets*nvol]
   const double *coef;          // shm [ntets][M][14] or fac [ntets][M][72]
-  int lattice;
+  int out_split;               // 1: rows / f addressed through vol_start
   double omega;
   const int *hp_ptr, *hp_code; // GS hyperplanes (hhg_smooth.cuh)
 };
@@ -98,53 +98,57 @@ __device__ __forceinline__ void ten_nodal_acc(double &acc, double &diag, const d
   }
 }
 
-// one row of the tensor operator at interior point (i, j, k) of element t.
-// GS=false: acc = sum_d s_d (v_d - v0).  GS=true: acc = sum_d s_d v_d and
-// diag = -sum_d s_d.  `ut` / `gt`: value arrays (interior block or lattice,
-// ghost shell), `kt`: the element's M component lattices.
-template <bool NODAL, bool GS>
+// component values of lattice point q: AOS = [L][M] (the batched device
+// layout, one 48-byte record per point: 3 x 16-byte loads), else [M][L]
+// (the reference's km layout, kept for the per-element ABI)
+template <bool AOS>
+__device__ __forceinline__ void ten_k6(const double *kt, int L, int q, double (&k)[kTenM]) {
+  if constexpr (AOS) {
+    const double2 *p = reinterpret_cast<const double2 *>(kt + kTenM * q);
+#pragma unroll
+    for (int h = 0; h < kTenM / 2; ++h) {
+      const double2 v = __ldg(p + h);
+      k[2 * h] = v.x;
+      k[2 * h + 1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < kTenM; ++m) k[m] = __ldg(kt + m * L + q);
+  }
+}
+
+// one row of the tensor operator at interior point (i, j, k) of element t,
+// all operands in the element's lattice arrays (`ut` values, `kt` the M
+// component lattices): every neighbour address is affine in i, so the row
+// constants hoist out of the i loop.  GS=false: acc = sum_d s_d (v_d - v0).
+// GS=true: acc = sum_d s_d v_d and diag = -sum_d s_d.
+template <bool NODAL, bool GS, bool AOS>
 __device__ __forceinline__ void ten_row(const TenDesc &D, const IncPlanes &P, int i, int j,
-                                        int k, const double *ut, const double *gt,
-                                        const double *kt, const double *sc, double *es,
-                                        int tid, int nth, double &acc, double &diag,
-                                        double &v0) {
-  const int n = D.n;
+                                        const double *ut, const double *kt, const double *sc,
+                                        double *es, int tid, int nth, double &acc,
+                                        double &diag, double &v0) {
   const int L = (int)D.L;
   const int kp = inc_koff(P, 1, i, j);
   int ko[14];
   double vq[14];
 #pragma unroll
   for (int d = 0; d < 14; ++d) {
-    const int dk = c_dirs_h(d, 2);
-    const int qi = i + c_dirs_h(d, 0), qj = j + c_dirs_h(d, 1);
-    ko[d] = inc_koff(P, dk + 1, qi, qj);
-    if (D.lattice) {
-      vq[d] = ut[ko[d]];
-    } else {
-      int off;
-      const bool in = inc_voff(P, dk + 1, n, qi, qj, k + dk, off);
-      vq[d] = in ? ut[off] : gt[off];
-    }
+    ko[d] = inc_koff(P, c_dirs_h(d, 2) + 1, i + c_dirs_h(d, 0), j + c_dirs_h(d, 1));
+    vq[d] = ut[ko[d]];
   }
-  if (D.lattice) {
-    v0 = ut[kp];
-  } else {
-    int off;
-    inc_voff(P, 1, n, i, j, k, off);
-    v0 = ut[off];
-  }
+  v0 = ut[kp];
   acc = 0.0;
   diag = 0.0;
   if constexpr (!NODAL) {
     double k0[kTenM];
-#pragma unroll
-    for (int m = 0; m < kTenM; ++m) k0[m] = __ldg(kt + m * L + kp);
+    ten_k6<AOS>(kt, L, kp, k0);
 #pragma unroll
     for (int d = 0; d < 14; ++d) {
-      double s = dmul(dadd(k0[0], __ldg(kt + ko[d])), sc[d]);
+      double kq[kTenM];
+      ten_k6<AOS>(kt, L, ko[d], kq);
+      double s = dmul(dadd(k0[0], kq[0]), sc[d]);
 #pragma unroll
-      for (int m = 1; m < kTenM; ++m)
-        s = dadd(s, dmul(dadd(k0[m], __ldg(kt + m * L + ko[d])), sc[m * 14 + d]));
+      for (int m = 1; m < kTenM; ++m) s = dadd(s, dmul(dadd(k0[m], kq[m]), sc[m * 14 + d]));
       if constexpr (GS) {
         acc = d == 0 ? dmul(s, vq[d]) : dadd(acc, dmul(s, vq[d]));
         diag = dsub(diag, s);
@@ -154,14 +158,18 @@ __device__ __forceinline__ void ten_row(const TenDesc &D, const IncPlanes &P, in
       }
     }
   } else {
-    // element sums of every component into this thread's smem column
+    // element sums of every component into this thread's smem column;
+    // per-point base pointers once, components at immediate offsets
+    const double *pq[15];
+    pq[0] = AOS ? kt + kTenM * kp : kt + kp;
+#pragma unroll
+    for (int d = 0; d < 14; ++d) pq[1 + d] = AOS ? kt + kTenM * ko[d] : kt + ko[d];
 #pragma unroll 1
     for (int m = 0; m < kTenM; ++m) {
-      const double *km = kt + m * L;
+      const int mo = AOS ? m : m * L;
       double b[55];
-      b[0] = __ldg(km + kp);
 #pragma unroll
-      for (int d = 0; d < 14; ++d) b[1 + d] = __ldg(km + ko[d]);
+      for (int x = 0; x < 15; ++x) b[x] = __ldg(pq[x] + mo);
       cse_steps<0>(b);
 #pragma unroll
       for (int e = 0; e < 24; ++e) es[(m * 24 + e) * nth + tid] = b[31 + e];
@@ -170,8 +178,10 @@ __device__ __forceinline__ void ten_row(const TenDesc &D, const IncPlanes &P, in
   }
 }
 
-// apply / residual: grid (k - 1, j band, element), block (32, rows)
-template <bool NODAL, bool RES>
+// apply / residual: grid (k - 1, j band, element), block (32, rows).
+// Inputs: lattice values D.u [ntets*L]; rows written to the global vector
+// (D.out_split: vol_start[t] + rank) or per element [ntets*nvol].
+template <bool NODAL, bool RES, bool AOS>
 __global__ void __launch_bounds__(ten_threads<NODAL>())
 tensor_volume_kernel(TenDesc D) {
   extern __shared__ double ten_sm[];
@@ -189,23 +199,23 @@ tensor_volume_kernel(TenDesc D) {
   if (j > n - 2 - k) return;
   const IncPlanes P = inc_planes(n, k);
   const double *kt = D.km + (long long)t * kTenM * D.L;
-  const double *ut = D.lattice ? D.u + (long long)t * D.L : D.u + D.vol_start[t];
-  const double *gt = D.lattice ? nullptr : D.ghost + (long long)t * D.S;
-  double *ot = D.lattice ? D.out + (long long)t * D.nvol : D.out + D.vol_start[t];
-  const double *ft = D.f ? (D.lattice ? D.f + (long long)t * D.nvol : D.f + D.vol_start[t])
-                         : nullptr;
+  const double *ut = D.u + (long long)t * D.L;
+  const long long o0 = D.out_split ? D.vol_start[t] : (long long)t * D.nvol;
+  double *ot = D.out + o0;
+  const double *ft = RES ? D.f + o0 : nullptr;
+  // volume rank of (i, j, k): inner-lattice row (k-1, j-1) + i - 1
+  const int c0 = P.ib[1] + (j - 1) * P.ri[1] - (j - 1) * (j - 2) / 2 - 1;
   for (int i = 1 + threadIdx.x; i <= n - 1 - k - j; i += 32) {
     double acc, diag, v0;
-    ten_row<NODAL, false>(D, P, i, j, k, ut, gt, kt, sc, es, tid, NT, acc, diag, v0);
-    int c;
-    inc_voff(P, 1, n, i, j, k, c);            // volume rank of (i, j, k)
-    ot[c] = RES ? dsub(ft[c], acc) : acc;
+    ten_row<NODAL, false, AOS>(D, P, i, j, ut, kt, sc, es, tid, NT, acc, diag, v0);
+    ot[c0 + i] = RES ? dsub(ft[c0 + i], acc) : acc;
   }
 }
 
-// forward Gauss-Seidel: one CTA per element walks the hyperplanes
-// h = i + 2j + 3k (bitwise the lexicographic sweep, see hhg_smooth.cuh)
-template <bool NODAL>
+// forward Gauss-Seidel on the lattice arrays: one CTA per element walks
+// the hyperplanes h = i + 2j + 3k (bitwise the lexicographic sweep, see
+// hhg_smooth.cuh); f is global (D.out_split) or per element
+template <bool NODAL, bool AOS>
 __global__ void __launch_bounds__(ten_threads<NODAL>())
 tensor_gs_kernel(TenDesc D) {
   extern __shared__ double ten_sm[];
@@ -220,10 +230,8 @@ tensor_gs_kernel(TenDesc D) {
   __syncthreads();
   const double omega = D.omega;
   const double *kt = D.km + (long long)t * kTenM * D.L;
-  double *ut = const_cast<double *>(D.lattice ? D.u + (long long)t * D.L
-                                              : D.u + D.vol_start[t]);
-  const double *gt = D.lattice ? nullptr : D.ghost + (long long)t * D.S;
-  const double *ft = D.lattice ? D.f + (long long)t * D.nvol : D.f + D.vol_start[t];
+  double *ut = const_cast<double *>(D.u) + (long long)t * D.L;
+  const double *ft = D.f + (D.out_split ? D.vol_start[t] : (long long)t * D.nvol);
   const int hmin = 6, hmax = 3 * n - 6;
   for (int h = hmin; h <= hmax; ++h) {
     const int ha = D.hp_ptr[h - hmin], hb = D.hp_ptr[h - hmin + 1];
@@ -232,15 +240,50 @@ tensor_gs_kernel(TenDesc D) {
       const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
       const IncPlanes P = inc_planes(n, k);
       double acc, diag, v0;
-      ten_row<NODAL, true>(D, P, i, j, k, ut, gt, kt, sc, es, tid, NT, acc, diag, v0);
+      ten_row<NODAL, true, AOS>(D, P, i, j, ut, kt, sc, es, tid, NT, acc, diag, v0);
       if (diag == 0.0) atomicOr(&g_status, 1);
-      int c;
-      inc_voff(P, 1, n, i, j, k, c);
-      const int pos = D.lattice ? inc_koff(P, 1, i, j) : c;
-      ut[pos] = dadd(dmul(dsub(1.0, omega), v0), ddiv(dmul(omega, dsub(ft[c], acc)), diag));
+      const int c = P.ib[1] + (j - 1) * P.ri[1] - (j - 1) * (j - 2) / 2 + i - 1;
+      ut[inc_koff(P, 1, i, j)] =
+          dadd(dmul(dsub(1.0, omega), v0), ddiv(dmul(omega, dsub(ft[c], acc)), diag));
     }
     __syncthreads();
   }
+}
+
+// element lattices from the split global layout: interior points from the
+// element's volume block, shell points from its compact ghost shell (the
+// reference's u[elem_gidx[t]], operators.py:383).  grid (k, j band, element)
+__global__ void __launch_bounds__(128)
+lattice_gather_kernel(TenDesc D, double *lat) {
+  const int n = D.n;
+  const int t = blockIdx.z;
+  const int k = blockIdx.x;
+  const int j = blockIdx.y * 4 + threadIdx.y;
+  if (j > n - k) return;
+  const IncPlanes P = inc_planes(n, k);
+  const double *vt = D.u + D.vol_start[t];
+  const double *gt = D.ghost + (long long)t * D.S;
+  double *lt = lat + (long long)t * D.L + inc_koff(P, 1, 0, j);
+  for (int i = threadIdx.x; i <= n - k - j; i += 32) {
+    int off;
+    const bool in = inc_voff(P, 1, n, i, j, k, off);
+    lt[i] = in ? vt[off] : gt[off];
+  }
+}
+
+// interior values back into the global vector after a lattice GS sweep
+// (operators.py:464-466); grid (k - 1, j band, element)
+__global__ void __launch_bounds__(128)
+lattice_scatter_kernel(TenDesc D, const double *lat, double *u) {
+  const int n = D.n;
+  const int t = blockIdx.z;
+  const int k = 1 + blockIdx.x;
+  const int j = 1 + blockIdx.y * 4 + threadIdx.y;
+  if (j > n - 2 - k) return;
+  const IncPlanes P = inc_planes(n, k);
+  const double *lt = lat + (long long)t * D.L + inc_koff(P, 1, 0, j);
+  double *vt = u + D.vol_start[t] + P.ib[1] + (j - 1) * P.ri[1] - (j - 1) * (j - 2) / 2 - 1;
+  for (int i = 1 + threadIdx.x; i <= n - 1 - k - j; i += 32) vt[i] = lt[i];
 }
 
 __constant__ int c_ten_tptr[15] = HHG_TPTR;
@@ -250,7 +293,7 @@ __constant__ int c_ten_telem[72] = HHG_TELEM;
 // of gs_surface_fill_kernel): per incidence and inside direction
 //   scaled: w_d = sum_m (k_m0 + k_md) psh_m[cls][d]
 //   nodal:  w_d = sum_{t in terms(d)} sum_m esum_m[telem[t]] pfac_m[cls][t]
-// psh: [ntets][M][14][14], pfac: [ntets][M][14][72], km: [ntets][M][L]
+// psh: [ntets][M][14][14], pfac: [ntets][M][14][72], km: [ntets][L][M]
 __global__ void tensor_surface_fill_kernel(SurfGSDesc G, const double *km) {
   const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const SurfDesc &D = G.s;
@@ -284,7 +327,7 @@ __global__ void tensor_surface_fill_kernel(SurfGSDesc G, const double *km) {
         double s = 0.0;
         for (int m = 0; m < kTenM; ++m) {
           const double *sh = D.psh + (((long long)t * kTenM + m) * 14 + cls) * 14;
-          const double x = dmul(dadd(kt[m * L + kp], kt[m * L + ko[d]]), sh[d]);
+          const double x = dmul(dadd(kt[kTenM * kp + m], kt[kTenM * ko[d] + m]), sh[d]);
           s = m == 0 ? x : dadd(s, x);
         }
         *val++ = s;
@@ -294,8 +337,8 @@ __global__ void tensor_surface_fill_kernel(SurfGSDesc G, const double *km) {
       double es[kTenM][24];
       for (int m = 0; m < kTenM; ++m) {
         double b[55];
-        b[0] = kt[m * L + kp];
-        for (int d = 0; d < 14; ++d) b[1 + d] = kt[m * L + ko[d]];
+        b[0] = kt[kTenM * kp + m];
+        for (int d = 0; d < 14; ++d) b[1 + d] = kt[kTenM * ko[d] + m];
         cse_steps<0>(b);
         for (int e = 0; e < 24; ++e) es[m][e] = b[31 + e];
       }

@@ -223,6 +223,15 @@ class Operator:
                          "sh": sh, "fac": fac, "km": km}
         return self._dev
 
+    def _lattice_work(self):
+        """Element-lattice scratch of the tensor kernels ([elements * L])."""
+        D = self._device()
+        if D.get("work") is None:
+            gt = D["grid"].gt
+            D["work"] = D["torch"].empty(max(gt.ntets * gt.L, 1), dtype=D["torch"].float64,
+                                         device="cuda")
+        return D["work"]
+
     def _vol_flags(self, residual=False):
         f = _lib.FLAG_RESIDUAL if residual else 0
         if self.is_tensor and self._stored is None:
@@ -291,7 +300,8 @@ class Operator:
             check(lib.hhg_tensor_volume_apply(dg.ref, self._vol_variant(), flags,
                                               self.coeff.M, D["km"].data_ptr(),
                                               D["coef"].data_ptr(), du.data_ptr(), fp,
-                                              out.data_ptr(), st), "tensor_volume_apply")
+                                              out.data_ptr(), self._lattice_work().data_ptr(),
+                                              st), "tensor_volume_apply")
         else:
             check(lib.hhg_volume_apply(dg.ref, self._vol_variant(), flags,
                                        D["coef"].data_ptr(), wp, du.data_ptr(), fp,
@@ -444,7 +454,9 @@ class Operator:
                 check(lib.hhg_tensor_smooth_volume(dg.ref, var, self.coeff.M,
                                                    D["km"].data_ptr(), coef.data_ptr(),
                                                    float(omega), du.data_ptr(),
-                                                   df.data_ptr(), st), "tensor_smooth_volume")
+                                                   df.data_ptr(),
+                                                   self._lattice_work().data_ptr(), st),
+                      "tensor_smooth_volume")
             D["torch"].cuda.current_stream().synchronize()
             check(lib.hhg_status(), "smooth")
             return du

@@ -99,7 +99,8 @@ def test_tensor_splitting_reconstructs_and_rejects():
     assert np.abs(K - Kfn(pts)).max() < 1e-13
     grid = M.RefinedGrid(M.unit_cube_6(), 1)
     tc = TensorCoefficient(grid, Kfn)
-    assert tc.M == 6 and tc.packed().shape == (6, 6, grid.lat.size)
+    assert tc.M == 6 and tc.packed().shape == (6, grid.lat.size, 6)
+    assert np.array_equal(tc.packed()[2, :, 4], tc.fields[4].values[2])
     assert np.abs(tc.reconstruct(pts) - Kfn(pts)).max() < 1e-13
 
     def bad(p):

@@ -109,12 +109,13 @@ if "stored" not in skip:
 
 if "tensor" not in skip:
     km = torch.empty(ne * 6 * L, dtype=torch.float64, device=dev).uniform_(0.5, 2.0)
+    work = torch.empty(ne * L, dtype=torch.float64, device=dev)
     for name, var, coef, flops in (("tensor scaling (M=6)", VAR["scaling"], shm, 14 * 20),
                                    ("tensor nodal (M=6)", VAR["nodal"], facm, 6 * 40 + 72 * 12 + 42)):
         nb = 7 * per_lat + rows_b
         ms = timed(lambda: check(lib.hhg_tensor_volume_apply(
             dg.ref, var, 0, 6, km.data_ptr(), coef.data_ptr(), u.data_ptr(), None,
-            out.data_ptr(), st)))
+            out.data_ptr(), work.data_ptr(), st)))
         results.append((name, ms, nb, flops))
         print(f"{name:40s} {ms:8.3f} ms {nrows / ms / 1e6:8.1f} GDoF/s "
               f"{nb / ms / 1e6:8.1f} GB/s {flops * nrows / ms / 1e9:8.2f} TFLOP/s", flush=True)
