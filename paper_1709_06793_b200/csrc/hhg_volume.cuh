@@ -599,11 +599,57 @@ __device__ __forceinline__ void mirror_seed(const Win<B> &lo, const Win<B> &mi,
 
 // rows of plane kk from windows mi (kk) and hi (kk+1) plus the carry;
 // leaves the carry for plane kk+1.  Accumulation order d = 0..13 exactly.
+#ifndef HHG_MIRROR_INTERLEAVE
+#define HHG_MIRROR_INTERLEAVE 0
+#endif
 template <int B>
 __device__ __forceinline__ void mirror_step(const Win<B> &mi, const Win<B> &hi,
                                             const double (&sh)[7], MirrorCarry<B> &c,
                                             double (&out)[B]) {
   double t1[B], n2[B], n12[B];
+#if HHG_MIRROR_INTERLEAVE
+  // direction-major: the B rows' terms of one direction side by side
+  double a[B];
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = edge_term<B>(mi.C[s + 1], mi.R[s + 1], sh[0]);      // d 0
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    t1[s] = edge_term<B>(mi.C[s + 1], mi.C[s + 2], sh[1]);                             // d 1
+    a[s] = dadd(a[s], t1[s]);
+  }
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    n2[s] = edge_term<B>(mi.C[s + 1], hi.C[s + 1], sh[2]);                             // d 2
+    a[s] = dadd(a[s], n2[s]);
+  }
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], mi.R[s], sh[3]));  // d 3
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], c.t4[s]);                              // d 4
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = (s + 1 < B) ? dsub(a[s], c.t12[s + 1]) : dadd(a[s], c.t5);  // d 5
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], hi.R[s], sh[6]));  // d 6
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], mi.L[s], sh[0]));  // d 7
+#pragma unroll
+  for (int s = 0; s < B; ++s)
+    a[s] = (s >= 1) ? dsub(a[s], t1[s - 1])
+                    : dadd(a[s], edge_term<B>(mi.C[s + 1], mi.C[s], sh[1]));            // d 8
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = dsub(a[s], c.t2[s]);                              // d 9
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], mi.L[s + 1], sh[3]));  // d 10
+#pragma unroll
+  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], hi.L[s], sh[4]));  // d 11
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    n12[s] = edge_term<B>(mi.C[s + 1], hi.C[s], sh[5]);                                // d 12
+    a[s] = dadd(a[s], n12[s]);
+  }
+#pragma unroll
+  for (int s = 0; s < B; ++s) out[s] = dadd(a[s], c.t13[s]);                           // d 13
+#else
 #pragma unroll
   for (int s = 0; s < B; ++s) {
     const double2 p = mi.C[s + 1];
@@ -627,6 +673,7 @@ __device__ __forceinline__ void mirror_step(const Win<B> &mi, const Win<B> &hi,
     a = dadd(a, c.t13[s]);                                          // d 13
     out[s] = a;
   }
+#endif
 #pragma unroll
   for (int s = 0; s < B; ++s) {
     c.t2[s] = n2[s];
