@@ -284,8 +284,13 @@ class Operator:
     def _stream(self):
         return self._device()["torch"].cuda.current_stream().cuda_stream
 
-    def apply_device(self, du, out=None, f=None):
-        """Device-resident A u (or f - A u when f is given), torch tensors."""
+    def apply_device(self, du, out=None, f=None, after_surface=None):
+        """Device-resident A u (or f - A u when f is given), torch tensors.
+
+        ``after_surface``: optional callable invoked once the surface and
+        Dirichlet rows are enqueued and before the volume rows are; the
+        sharded operator hangs its interface exchange there so it overlaps
+        the volume kernel (surface and volume rows are disjoint)."""
         D = self._device()
         torch = D["torch"]
         if out is None:
@@ -295,6 +300,9 @@ class Operator:
         flags = self._vol_flags(residual=f is not None)
         fp = f.data_ptr() if f is not None else None
         check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
+        if after_surface is not None:
+            self._surface(dg, ds, flags & _lib.FLAG_RESIDUAL, du, fp, out, st)
+            after_surface(out)
         wp = D["w"].data_ptr() if D["w"] is not None else None
         if self.is_tensor and self._stored is None:
             check(lib.hhg_tensor_volume_apply(dg.ref, self._vol_variant(), flags,
@@ -306,7 +314,8 @@ class Operator:
             check(lib.hhg_volume_apply(dg.ref, self._vol_variant(), flags,
                                        D["coef"].data_ptr(), wp, du.data_ptr(), fp,
                                        out.data_ptr(), st), "volume_apply")
-        self._surface(dg, ds, flags & _lib.FLAG_RESIDUAL, du, fp, out, st)
+        if after_surface is None:
+            self._surface(dg, ds, flags & _lib.FLAG_RESIDUAL, du, fp, out, st)
         self._count()
         return out
 

@@ -24,7 +24,8 @@ import numpy as np
 
 from .mesh import MacroMesh, kuhn_blocks
 
-__all__ = ["slab_mesh", "InterfaceMap", "exchange_partials", "owned_mask"]
+__all__ = ["slab_mesh", "InterfaceMap", "exchange_partials", "owned_mask",
+           "ShardedOperator", "sharded_cg"]
 
 
 def slab_mesh(rank: int, world: int, nx: int = 4, ny: int = 4) -> MacroMesh:
@@ -104,3 +105,98 @@ def exchange_partials(out, imap: InterfaceMap, dist, index_tensors=None):
         total = (theirs + mine) if nbr < imap.rank else (mine + theirs)
         out.index_copy_(0, ids_t[nbr], total)
     return out
+
+
+class ShardedOperator:
+    """One rank's share of a partitioned operator: the local slab operator
+    plus the interface exchange.
+
+    ``op`` is the rank's :class:`~.operators.Operator` (device path) or, for
+    the CPU multi-process tests, any object with ``apply(u) -> ndarray`` on
+    the rank's local numbering.  Vectors are torch tensors (CUDA for the
+    device path, CPU for gloo).  On the device the surface rows are launched
+    first and the exchange runs on a side stream while the volume kernel
+    computes the (communication-free) volume rows."""
+
+    def __init__(self, op, imap: InterfaceMap, dist, dirichlet_mask):
+        import torch
+        self.op, self.imap, self.dist = op, imap, dist
+        self.torch = torch
+        self._idx, self._side, self._masks = {}, None, {}
+        self._dirichlet = np.asarray(dirichlet_mask, dtype=bool)
+        self._owned = imap.owned_mask(len(self._dirichlet)) & ~self._dirichlet
+
+    def _index(self, device):
+        key = str(device)
+        if key not in self._idx:
+            self._idx[key] = {k: self.torch.as_tensor(v, device=device)
+                              for k, v in self.imap.neighbours.items()}
+        return self._idx[key]
+
+    def _mask(self, name, device):
+        key = (name, str(device))
+        if key not in self._masks:
+            m = self._owned if name == "owned" else ~self._dirichlet
+            self._masks[key] = self.torch.as_tensor(m.astype(np.float64), device=device)
+        return self._masks[key]
+
+    def apply(self, u):
+        """A u with the interface rows completed (identity Dirichlet rows)."""
+        torch = self.torch
+        if u.is_cuda and hasattr(self.op, "apply_device"):
+            idx = self._index(u.device)
+            if self._side is None:
+                self._side = torch.cuda.Stream()
+            side, main = self._side, torch.cuda.current_stream()
+
+            def exchange(out):
+                ev = torch.cuda.Event()
+                ev.record(main)
+                with torch.cuda.stream(side):
+                    side.wait_event(ev)
+                    exchange_partials(out, self.imap, self.dist, idx)
+
+            out = self.op.apply_device(u, after_surface=exchange)
+            main.wait_stream(side)
+            return out
+        out = torch.from_numpy(np.asarray(self.op.apply(u.numpy()), dtype=np.float64))
+        return exchange_partials(out, self.imap, self.dist, self._index(out.device))
+
+    def residual(self, u, f):
+        """f - A u, zero on Dirichlet rows."""
+        return (f - self.apply(u)) * self._mask("free", u.device)
+
+    def dot(self, a, b):
+        """Global dot: every shared node counted once (owner = lower rank),
+        Dirichlet entries excluded, one all-reduce."""
+        local = (a * b * self._mask("owned", a.device)).sum().reshape(1)
+        self.dist.all_reduce(local)
+        return local
+
+
+def sharded_cg(sop: ShardedOperator, f, tol=1e-10, max_iter=10000):
+    """Plain CG on the partitioned system (the reference's _cg,
+    multigrid.py:169-194, with global dots): stop when ||r|| <= tol ||b||.
+    Returns (x, iterations, final residual norm)."""
+    torch = sop.torch
+    free = sop._mask("free", f.device)
+    x = torch.zeros_like(f)
+    r = f * free
+    p = r.clone()
+    rs = sop.dot(r, r)
+    b0 = float(torch.sqrt(rs).item())
+    if b0 == 0.0:
+        return x, 0, 0.0
+    it, res = 0, b0
+    for it in range(1, max_iter + 1):
+        Ap = sop.apply(p) * free
+        alpha = rs / sop.dot(p, Ap)
+        x = x + alpha * p
+        r = r - alpha * Ap
+        rs_new = sop.dot(r, r)
+        res = float(torch.sqrt(rs_new).item())
+        if res <= tol * b0:
+            break
+        p = r + (rs_new / rs) * p
+        rs = rs_new
+    return x, it, res
