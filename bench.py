@@ -153,39 +153,20 @@ def run_own(args):
     t_setup = time.time() - t_setup
 
     vol_ev = []
-    side = torch.cuda.Stream() if imap is not None else None
 
     def step(record=False):
-        # identical to Operator.apply_device, with CUDA events around the
-        # volume kernel on the launching stream
-        from paper_1709_06793_b200 import _lib
-        from paper_1709_06793_b200._lib import check
-        st = torch.cuda.current_stream()
-        s = st.cuda_stream
-        dg, ds = D["grid"], D["surf"]
-        flags = op._vol_flags()
-        check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), s))
+        # the product's Operator.apply_device (surface rows + the N>1
+        # interface exchange on a side stream, concurrent with the ghost
+        # update and the volume kernel), with CUDA events around the volume
+        # kernel on the launching stream
+        ev = None
+        if record:
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            vol_ev.append(ev)
+        hook = None
         if imap is not None:
-            # N > 1: surface rows first, their interface exchange on a side
-            # stream overlapping the volume kernel (ShardedOperator.apply)
-            op._surface(dg, ds, 0, du, None, out, s)
-            ev = torch.cuda.Event()
-            ev.record(st)
-            with torch.cuda.stream(side):
-                side.wait_event(ev)
-                exchange_partials(out, imap, dist, idx_t)
-        if record:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-        check(lib.hhg_volume_apply(dg.ref, op._vol_variant(), flags, D["coef"].data_ptr(),
-                                   None, du.data_ptr(), None, out.data_ptr(), s))
-        if record:
-            e1.record(st)
-            vol_ev.append((e0, e1))
-        if imap is None:
-            op._surface(dg, ds, 0, du, None, out, s)
-        else:
-            st.wait_stream(side)
+            hook = lambda o: exchange_partials(o, imap, dist, idx_t)  # noqa: E731
+        op.apply_device(du, out=out, after_surface=hook, volume_events=ev)
 
     for _ in range(args.warmup):
         step()

@@ -122,7 +122,7 @@ class ShardedOperator:
         import torch
         self.op, self.imap, self.dist = op, imap, dist
         self.torch = torch
-        self._idx, self._side, self._masks = {}, None, {}
+        self._idx, self._masks = {}, {}
         self._dirichlet = np.asarray(dirichlet_mask, dtype=bool)
         self._owned = imap.owned_mask(len(self._dirichlet)) & ~self._dirichlet
 
@@ -145,20 +145,10 @@ class ShardedOperator:
         torch = self.torch
         if u.is_cuda and hasattr(self.op, "apply_device"):
             idx = self._index(u.device)
-            if self._side is None:
-                self._side = torch.cuda.Stream()
-            side, main = self._side, torch.cuda.current_stream()
-
-            def exchange(out):
-                ev = torch.cuda.Event()
-                ev.record(main)
-                with torch.cuda.stream(side):
-                    side.wait_event(ev)
-                    exchange_partials(out, self.imap, self.dist, idx)
-
-            out = self.op.apply_device(u, after_surface=exchange)
-            main.wait_stream(side)
-            return out
+            # runs on the operator's side stream right after the surface
+            # rows, concurrently with the volume kernel
+            return self.op.apply_device(
+                u, after_surface=lambda out: exchange_partials(out, self.imap, self.dist, idx))
         out = torch.from_numpy(np.asarray(self.op.apply(u.numpy()), dtype=np.float64))
         return exchange_partials(out, self.imap, self.dist, self._index(out.device))
 
