@@ -759,13 +759,14 @@ volume_kernel_mirror(VolDesc D) {
     const int sl = p % NS;
     if (p >= NS && !empty_ok) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
     const unsigned off = ring_s + (unsigned)sl * PLANE_BYTES;
+    const bool copy = HHG_VOL_EXPT != 2 || p < PD;   // EXPT 2: arithmetic only
 #pragma unroll
     for (int m = 0; m < NSLOT; ++m) {
       IncSlot &S = sl_[m];
       const int si = S.ij & 0xffff, sj = S.ij >> 16;
       {
         // predicated copies instead of a divergent branch per slot
-        const int live = p <= S.pmax;
+        const int live = copy && p <= S.pmax;
         const bool interior = p >= 1 && si >= 1 && sj >= 1 && p < S.pmax;
         const double *vs = interior ? at(T.v, S.vo) : at(T.g, S.go);
         const double *ks = at(T.k, S.ko);
@@ -846,7 +847,12 @@ volume_kernel_mirror(VolDesc D) {
     fetch(q, hi);
     if (warp_min_ij <= n - q) {   // some lane of the warp is valid
       double vals[B];
-      mirror_step<B>(mi, hi, sh, carry, vals);
+      if constexpr (HHG_VOL_EXPT == 1) {          // data movement only
+#pragma unroll
+        for (int s = 0; s < B; ++s) vals[s] = hi.C[s + 1].x + mi.R[s].y + mi.L[s + 1].x;
+      } else {
+        mirror_step<B>(mi, hi, sh, carry, vals);
+      }
       emit(q - 1, vals);
     }
     refill(q);
