@@ -31,6 +31,10 @@ extern "C" {
 
 #define HHG_OK 0
 #define HHG_ERR_ARG (-1)
+/* largest supported lattice size n = 2^level (level 9): lattice offsets are
+ * 32-bit closed forms and point codes pack i, j, k in 10 bits each; every
+ * entry point returns HHG_ERR_ARG for larger n */
+#define HHG_MAX_N 512
 #define HHG_ERR_CUDA (-2)
 #define HHG_ERR_ZERO_DIAG (-3)
 #define HHG_ERR_TABLE (-4)

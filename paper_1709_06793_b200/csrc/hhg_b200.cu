@@ -199,6 +199,7 @@ extern "C" {
 
 int hhg_apply_scaling_3d(int64_t n, const int64_t *, const double *v, const double *kc,
                          const double *sh, double *out, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (n < 4) return HHG_OK;
   VolDesc D = elem_desc(n, v, kc, sh, 14, out);
   int rc = elem_tiles((int)n, &D.tiles, &D.ntiles);
@@ -210,6 +211,7 @@ int hhg_apply_nodal_3d(int64_t n, const int64_t *, const double *v, const double
                        const int64_t *sched, int64_t nsched, const int64_t *sums,
                        const double *fac, const int64_t *tptr, const int64_t *telem,
                        double *out, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
   if (n < 4) return HHG_OK;
   VolDesc D = elem_desc(n, v, kc, fac, 72, out);
@@ -220,6 +222,7 @@ int hhg_apply_nodal_3d(int64_t n, const int64_t *, const double *v, const double
 
 int hhg_apply_const_3d(int64_t n, const int64_t *, const double *v, const double *s15,
                        double, double *out, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   // s15: 14 neighbour weights followed by c0 (device); the c0 argument is
   // accepted for signature parity and must equal s15[14]
   if (n < 4) return HHG_OK;
@@ -231,6 +234,7 @@ int hhg_apply_const_3d(int64_t n, const int64_t *, const double *v, const double
 
 int hhg_apply_stored_3d(int64_t n, const int64_t *, const double *v, const double *w,
                         double *out, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (n < 4) return HHG_OK;
   VolDesc D = elem_desc(n, v, v, nullptr, 0, out);
   D.w = w;
@@ -298,6 +302,7 @@ static int gs_elem(int var, int64_t n, double *u, const double *fv, const double
 
 int hhg_gs_scaling_3d(int64_t n, const int64_t *, double *u, const double *fv,
                       const double *kc, const double *sh, double omega, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   return gs_elem(0, n, u, fv, kc, sh, 14, omega, S(stream));
 }
 
@@ -305,6 +310,7 @@ int hhg_gs_nodal_3d(int64_t n, const int64_t *, double *u, const double *fv,
                     const double *kc, const int64_t *sched, int64_t nsched,
                     const int64_t *sums, const double *fac, const int64_t *tptr,
                     const int64_t *telem, double omega, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
   return gs_elem(1, n, u, fv, kc, fac, 72, omega, S(stream));
 }
@@ -329,6 +335,7 @@ static VolDesc grid_desc(const hhg_grid *g) {
 }
 
 int hhg_ghost_update(const hhg_grid *g, const double *u, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   const long long total = (long long)g->ntets * g->shell_size;
   if (total == 0) return HHG_OK;
   int blocks = (int)((total + 255) / 256);
@@ -341,6 +348,7 @@ int hhg_ghost_update(const hhg_grid *g, const double *u, void *stream) {
 int hhg_volume_apply(const hhg_grid *g, int variant, int flags, const double *coef,
                      const double *w, const double *u, const double *f, double *out,
                      void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (g->n < 4 || g->ntiles == 0) return HHG_OK;
   VolDesc D = grid_desc(g);
   D.u = u;
@@ -382,6 +390,7 @@ static SurfDesc surf_desc(const hhg_grid *g, const hhg_surface *s) {
 
 int hhg_surface_apply(const hhg_grid *g, const hhg_surface *s, int, int flags,
                       const double *u, const double *f, double *out, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   const bool res = flags & HHG_FLAG_RESIDUAL;
   SurfDesc D = surf_desc(g, s);
   D.u = u;
@@ -415,6 +424,7 @@ int hhg_surface_apply(const hhg_grid *g, const hhg_surface *s, int, int flags,
 int hhg_smooth_surface_level(const hhg_grid *g, const hhg_surface *s,
                              const int64_t *level_rows, int64_t count, double omega,
                              double *u, const double *f, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (count <= 0) return HHG_OK;
   SurfGSDesc G{};
   G.s = surf_desc(g, s);
@@ -431,6 +441,7 @@ int hhg_smooth_surface_level(const hhg_grid *g, const hhg_surface *s,
 // surface rows of the smoother, precomputed once: weights + diagonals
 int hhg_smooth_surface_prepare(const hhg_grid *g, const hhg_surface *s,
                                const hhg_surface_gs *gs, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (s->nrows <= 0) return HHG_OK;
   SurfGSDesc G{};
   G.s = surf_desc(g, s);
@@ -447,6 +458,7 @@ int hhg_smooth_surface_prepare(const hhg_grid *g, const hhg_surface *s,
 int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
                           int flags, const double *u, const double *f, double *out,
                           void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   const bool res = flags & HHG_FLAG_RESIDUAL;
   SurfGSDesc G{};
   G.s = surf_desc(g, s);
@@ -476,6 +488,7 @@ int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s, const hhg_sur
 // sized to the mean level width (a narrow sweep syncs few blocks)
 int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
                            double omega, double *u, const double *f, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (gs->nlev <= 0) return HHG_OK;
   SurfGSDesc G{};
   G.s = surf_desc(g, s);
@@ -516,6 +529,7 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_su
 
 int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double omega,
                       double *u, const double *f, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (g->n < 4) return HHG_OK;
   GSDesc G{};
   G.n = g->n;
@@ -631,6 +645,7 @@ extern "C" {
 int hhg_apply_scaling_tensor_3d(int64_t n, const int64_t *, const double *v,
                                 const double *km, int64_t M, const double *shm,
                                 double *out, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (M != kTenM) return HHG_ERR_ARG;
   TenDesc D = ten_elem(n, v, km, shm);
   D.out = out;
@@ -641,6 +656,7 @@ int hhg_apply_nodal_tensor_3d(int64_t n, const int64_t *, const double *v, const
                               int64_t M, const int64_t *sched, int64_t nsched,
                               const int64_t *sums, const double *fac, const int64_t *tptr,
                               const int64_t *telem, double *out, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (M != kTenM) return HHG_ERR_ARG;
   if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
   TenDesc D = ten_elem(n, v, km, fac);
@@ -651,6 +667,7 @@ int hhg_apply_nodal_tensor_3d(int64_t n, const int64_t *, const double *v, const
 int hhg_gs_scaling_tensor_3d(int64_t n, const int64_t *, double *u, const double *fv,
                              const double *km, int64_t M, const double *shm, double omega,
                              void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (M != kTenM) return HHG_ERR_ARG;
   TenDesc D = ten_elem(n, u, km, shm);
   D.f = fv;
@@ -662,6 +679,7 @@ int hhg_gs_nodal_tensor_3d(int64_t n, const int64_t *, double *u, const double *
                            const double *km, int64_t M, const int64_t *sched, int64_t nsched,
                            const int64_t *sums, const double *fac, const int64_t *tptr,
                            const int64_t *telem, double omega, void *stream) {
+  if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (M != kTenM) return HHG_ERR_ARG;
   if (!tables_match(sched, nsched, sums, tptr, telem)) return HHG_ERR_TABLE;
   TenDesc D = ten_elem(n, u, km, fac);
@@ -673,6 +691,7 @@ int hhg_gs_nodal_tensor_3d(int64_t n, const int64_t *, double *u, const double *
 int hhg_tensor_volume_apply(const hhg_grid *g, int variant, int flags, int M,
                             const double *km, const double *coef, const double *u,
                             const double *f, double *out, double *work, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (M != kTenM || !work) return HHG_ERR_ARG;
   if (variant != HHG_VAR_SCALING && variant != HHG_VAR_NODAL) return HHG_ERR_ARG;
   const bool res = (flags & HHG_FLAG_RESIDUAL) != 0;
@@ -691,6 +710,7 @@ int hhg_tensor_volume_apply(const hhg_grid *g, int variant, int flags, int M,
 int hhg_tensor_smooth_volume(const hhg_grid *g, int variant, int M, const double *km,
                              const double *coef, double omega, double *u, const double *f,
                              double *work, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (M != kTenM || !work) return HHG_ERR_ARG;
   if (variant != HHG_VAR_SCALING && variant != HHG_VAR_NODAL) return HHG_ERR_ARG;
   if (g->n < 4) return HHG_OK;
@@ -711,6 +731,7 @@ int hhg_tensor_smooth_volume(const hhg_grid *g, int variant, int M, const double
 int hhg_tensor_surface_prepare(const hhg_grid *g, const hhg_surface *s,
                                const hhg_surface_gs *gs, int M, const double *km,
                                void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (M != kTenM) return HHG_ERR_ARG;
   if (s->nrows <= 0) return HHG_OK;
   SurfGSDesc G{};

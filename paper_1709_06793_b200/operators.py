@@ -36,6 +36,7 @@ from .reference_stencils import (classify_edge_types, environment,
 __all__ = ["Operator", "VARIANTS", "parse_hybrid_set"]
 
 VARIANTS = ("const", "nodal", "scaling", "scaling_ma2", "hybrid", "stored")
+MAX_LEVEL = 9     # include/hhg_b200.h HHG_MAX_N = 512
 
 _KIND_NAMES = {"wv": PrimitiveKind.VERTEX, "we": PrimitiveKind.EDGE,
                "wf": PrimitiveKind.FACE}
@@ -99,6 +100,10 @@ class Operator:
                 raise ValueError("coefficient sampled on a different grid")
         if grid.dim != 3:
             raise ValueError("the B200 operators are tetrahedral (dim 3)")
+        if grid.level > MAX_LEVEL:
+            raise ValueError(f"refinement level {grid.level} exceeds the B200 build's "
+                             f"maximum {MAX_LEVEL} (n = 2^level <= 512: 32-bit lattice "
+                             "offsets, 10-bit point codes)")
         self._env = environment(3)
         self._nvol = grid.nodes_per_volume
         self._setup_tables()
