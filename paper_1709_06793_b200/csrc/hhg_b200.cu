@@ -195,6 +195,43 @@ static bool tables_match(const int64_t *sched, int64_t nsched, const int64_t *su
   return true;
 }
 
+// Volume Gauss-Seidel of all elements: cpt co-resident CTAs per element
+// (cooperative launch, grid barrier per hyperplane) when the device can hold
+// at least two per element, else one CTA per element (block barrier).
+template <int VAR>
+static int launch_gs_volume(GSDesc G, cudaStream_t st) {
+  static int capacity = 0;
+  if (capacity == 0) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gs_volume_kernel<VAR, true>,
+                                                  gs_volume_threads<VAR, true>(), 0);
+    capacity = sms * (per > 0 ? per : 1);
+  }
+  // enough CTAs per element to give each thread about one point per
+  // hyperplane, within the co-residency limit; the grid barrier (~2 us per
+  // hyperplane) and L1-bypassing loads do not pay for narrow hyperplanes
+  // (level 6: one CTA per element with L1-cached loads is faster)
+  constexpr int TC = gs_volume_threads<VAR, true>();
+  const long long avg = G.nvol / (3LL * G.n - 11);
+  const int cpt = G.ntets > 0 ? capacity / G.ntets : 1;
+  if (avg < 3LL * TC || cpt < 2) {
+    G.cpt = 1;
+    gs_volume_kernel<VAR, false><<<G.ntets, gs_volume_threads<VAR, false>(), 0, st>>>(G);
+    return check("gs_volume_kernel");
+  }
+  G.cpt = cpt;
+  void *args[] = {(void *)&G};
+  cudaError_t e = cudaLaunchCooperativeKernel((void *)gs_volume_kernel<VAR, true>,
+                                              G.ntets * cpt, TC, args, 0, st);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "hhg_b200: gs_volume_kernel (cooperative): %s\n", cudaGetErrorString(e));
+    return HHG_ERR_CUDA;
+  }
+  return HHG_OK;
+}
+
 extern "C" {
 
 int hhg_apply_scaling_3d(int64_t n, const int64_t *, const double *v, const double *kc,
@@ -295,8 +332,9 @@ static int gs_elem(int var, int64_t n, double *u, const double *fv, const double
   G.lattice = 1;
   int rc = hyperplanes((int)n, &G.hp_ptr, &G.hp_code);
   if (rc) return rc;
-  if (var == 0) gs_volume_kernel<0><<<1, gs_volume_threads<0>(), 0, st>>>(G);
-  else gs_volume_kernel<1><<<1, gs_volume_threads<1>(), 0, st>>>(G);
+  G.cpt = 1;
+  if (var == 0) gs_volume_kernel<0, false><<<1, gs_volume_threads<0, false>(), 0, st>>>(G);
+  else gs_volume_kernel<1, false><<<1, gs_volume_threads<1, false>(), 0, st>>>(G);
   return check("gs_volume_kernel");
 }
 
@@ -549,11 +587,8 @@ int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double
   G.lattice = 0;
   int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code);
   if (rc) return rc;
-  if (variant == HHG_VAR_NODAL)
-    gs_volume_kernel<1><<<g->ntets, gs_volume_threads<1>(), 0, S(stream)>>>(G);
-  else
-    gs_volume_kernel<0><<<g->ntets, gs_volume_threads<0>(), 0, S(stream)>>>(G);
-  return check("gs_volume_kernel");
+  return variant == HHG_VAR_NODAL ? launch_gs_volume<1>(G, S(stream))
+                                  : launch_gs_volume<0>(G, S(stream));
 }
 
 // ---------------------------------------------------------------------------

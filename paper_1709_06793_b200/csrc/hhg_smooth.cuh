@@ -37,6 +37,7 @@ struct GSDesc {
   int lattice;                 // 1: per-element lattice arrays
   const int *hp_ptr;           // [3n-4] hyperplane h = 6 + idx -> point range
   const int *hp_code;          // [nvol] i | j << 10 | k << 20, by hyperplane
+  int cpt;                     // CTAs per element (> 1: cooperative launch)
 };
 
 __device__ __forceinline__ double *gs_addr(const GSDesc &D, int t, int i, int j,
@@ -58,13 +59,23 @@ __device__ __forceinline__ double *gs_addr(const GSDesc &D, int t, int i, int j,
 }
 
 // block size: the nodal row's 55-slot buffer needs > 64 registers
-template <int VAR>
-constexpr int gs_volume_threads() { return VAR == 0 ? 512 : 256; }
+template <int VAR, bool COOP>
+constexpr int gs_volume_threads() { return (VAR == 0 ? 512 : 256) / (COOP ? 2 : 1); }
 
-template <int VAR>
-__global__ void __launch_bounds__(gs_volume_threads<VAR>())
+// One macro element per CTA group: D.cpt co-resident CTAs share an
+// element (blockIdx.x = t * cpt + c) and split every hyperplane's points;
+// a barrier separates the hyperplanes - the CTA barrier when cpt == 1,
+// else a grid-wide barrier of the cooperative launch (the sweep stays
+// bitwise the lexicographic one: points of one hyperplane are independent,
+// and all elements' volume rows are independent given the ghost shells).
+// Values another CTA wrote in the previous hyperplane are read with
+// ld.global.cg (no stale L1 copy); own-element k is read-only.
+template <int VAR, bool COOP>
+__global__ void __launch_bounds__(gs_volume_threads<VAR, COOP>(), COOP ? 2 : 1)
 gs_volume_kernel(GSDesc D) {
-  const int t = blockIdx.x;
+  const int cpt = COOP ? D.cpt : 1;
+  const int t = blockIdx.x / cpt;
+  const int part = blockIdx.x - t * cpt;
   const int n = D.n;
   if (n < 4) return;
   __shared__ double sfac[72];
@@ -80,9 +91,11 @@ gs_volume_kernel(GSDesc D) {
   const double omega = D.omega;
   const int hmin = 6, hmax = 3 * n - 6;
   const double *kt = D.kc + (long long)t * D.L;
+  const int stride = cpt * blockDim.x;
+  const int first = part * blockDim.x + threadIdx.x;
   for (int h = hmin; h <= hmax; ++h) {
     const int ha = D.hp_ptr[h - hmin], hb = D.hp_ptr[h - hmin + 1];
-    for (int e = ha + threadIdx.x; e < hb; e += blockDim.x) {
+    for (int e = ha + first; e < hb; e += stride) {
       const int code = __ldg(D.hp_code + e);
       const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
       // 32-bit plane constants of planes k-1, k, k+1 (as the surface rows)
@@ -97,7 +110,7 @@ gs_volume_kernel(GSDesc D) {
         inc_voff(P, 1, n, i, j, k, off);              // interior point
         up = ut + off;
       }
-      const double k0 = kt[inc_koff(P, 1, i, j)];
+      const double k0 = __ldg(kt + inc_koff(P, 1, i, j));
       double2 q[14];
 #pragma unroll
       for (int d = 0; d < 14; ++d) {
@@ -105,13 +118,13 @@ gs_volume_kernel(GSDesc D) {
         const int qi = i + c_dirs_h(d, 0), qj = j + c_dirs_h(d, 1), qk = k + dk;
         const int ko = inc_koff(P, dk + 1, qi, qj);
         if (D.lattice) {
-          q[d].x = ut[ko];
+          q[d].x = COOP ? __ldcg(ut + ko) : ut[ko];
         } else {
           int off;
           const bool in = inc_voff(P, dk + 1, n, qi, qj, qk, off);
-          q[d].x = in ? ut[off] : gt[off];
+          q[d].x = in ? (COOP ? __ldcg(ut + off) : ut[off]) : __ldg(gt + off);
         }
-        q[d].y = kt[ko];
+        q[d].y = __ldg(kt + ko);
       }
       double acc = 0.0, diag = 0.0;
       if (VAR == 0) {
@@ -130,9 +143,11 @@ gs_volume_kernel(GSDesc D) {
       const long long c = lbase32(n - 4, k - 1, j - 1) + i - 1;
       const double fv = D.lattice ? D.f[(long long)t * D.nvol + c]
                                   : D.f[D.vol_start[t] + c];
-      *up = dadd(dmul(dsub(1.0, omega), *up), ddiv(dmul(omega, dsub(fv, acc)), diag));
+      const double old = COOP ? __ldcg(up) : *up;
+      *up = dadd(dmul(dsub(1.0, omega), old), ddiv(dmul(omega, dsub(fv, acc)), diag));
     }
-    __syncthreads();
+    if constexpr (COOP) cooperative_groups::this_grid().sync();
+    else __syncthreads();
   }
 }
 
