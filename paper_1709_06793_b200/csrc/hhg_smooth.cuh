@@ -373,10 +373,57 @@ gs_surface_block_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
   }
 }
 
+// Row of the surface sweep split in two: everything that does not depend
+// on u (row id, entry range, diagonal, f, the first PF column ids and
+// weights) is fetched before the grid barrier that precedes the row's
+// level, so after the barrier only the neighbour values remain to be read.
+constexpr int kSurfPF = 24;   // face rows have ~24 entries
+struct SurfRowPF {
+  long long gid, e0, e1;
+  double diag, fv;
+  int col[kSurfPF];
+  double val[kSurfPF];
+};
+
+__device__ __forceinline__ void surf_row_prefetch(const SurfGSDesc &G, long long r,
+                                                  SurfRowPF &p) {
+  const SurfDesc &D = G.s;
+  p.gid = __ldg(D.rows + r);
+  p.e0 = __ldg(G.ent_ptr + r);
+  p.e1 = __ldg(G.ent_ptr + r + 1);
+  p.diag = __ldg(G.row_diag + r);
+  p.fv = __ldg(D.f + p.gid);
+#pragma unroll
+  for (int m = 0; m < kSurfPF; ++m)
+    if (p.e0 + m < p.e1) {
+      p.col[m] = __ldg(G.ent_col + p.e0 + m);
+      p.val[m] = __ldg(G.ent_val + p.e0 + m);
+    }
+}
+
+__device__ __forceinline__ void surf_row_finish(const SurfGSDesc &G, const SurfRowPF &p) {
+  double *u = const_cast<double *>(G.s.u);
+  double x[kSurfPF];
+#pragma unroll
+  for (int m = 0; m < kSurfPF; ++m)
+    if (p.e0 + m < p.e1) x[m] = __ldcg(u + (unsigned)p.col[m]);
+  const double old = __ldcg(u + p.gid);
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < kSurfPF; ++m)
+    if (p.e0 + m < p.e1) acc = dadd(acc, dmul(p.val[m], x[m]));
+  for (long long e = p.e0 + kSurfPF; e < p.e1; ++e)
+    acc = dadd(acc, dmul(__ldg(G.ent_val + e), __ldcg(u + (unsigned)__ldg(G.ent_col + e))));
+  if (p.diag == 0.0) atomicOr(&g_status, 1);
+  const double om = G.omega;
+  u[p.gid] = dadd(dmul(dsub(1.0, om), old), ddiv(dmul(om, dsub(p.fv, acc)), p.diag));
+}
+
 // all levels in one cooperative launch: rows of a level are spread over the
 // grid, a grid-wide barrier (with its memory fence) separates the levels;
 // neighbour values are read with ld.global.cg so no stale L1 copy survives
-// a level boundary
+// a level boundary.  Each thread's first row of the next level is
+// prefetched (surf_row_prefetch) before the barrier.
 __global__ void __launch_bounds__(64)
 gs_surface_all_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
@@ -384,9 +431,27 @@ gs_surface_all_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
   // spreads over all participating SMs
   const long long tid = threadIdx.x * (long long)gridDim.x + blockIdx.x;
   const long long nth = (long long)gridDim.x * blockDim.x;
+  SurfRowPF pf;
+  bool have = false;
+  if (nlev > 0 && level_ptr[0] + tid < level_ptr[1]) {
+    surf_row_prefetch(G, G.level_rows[level_ptr[0] + tid], pf);
+    have = true;
+  }
   for (int lv = 0; lv < nlev; ++lv) {
     const long long a = level_ptr[lv], b = level_ptr[lv + 1];
-    for (long long e = a + tid; e < b; e += nth) gs_surface_row_csr(G, G.level_rows[e]);
+    if (have) surf_row_finish(G, pf);
+    for (long long e = a + tid + nth; e < b; e += nth) {
+      surf_row_prefetch(G, G.level_rows[e], pf);
+      surf_row_finish(G, pf);
+    }
+    have = false;
+    if (lv + 1 < nlev) {
+      const long long e = level_ptr[lv + 1] + tid;
+      if (e < level_ptr[lv + 2]) {
+        surf_row_prefetch(G, G.level_rows[e], pf);
+        have = true;
+      }
+    }
     grid.sync();
   }
 }
