@@ -21,6 +21,8 @@ from __future__ import annotations
 import ctypes
 from functools import lru_cache
 
+import warnings
+
 import numpy as np
 
 from ._lib import HhgGrid, HhgSurface, lib
@@ -225,8 +227,12 @@ class DeviceGrid:
         torch = require_cuda()
         dev = torch.device("cuda")
         self.gt = gt
-        t = lambda a, dt=None: torch.as_tensor(np.ascontiguousarray(a), device=dev) \
-            if dt is None else torch.as_tensor(np.ascontiguousarray(a, dtype=dt), device=dev)
+        def t(a, dt=None):
+            a = np.ascontiguousarray(a) if dt is None else np.ascontiguousarray(a, dtype=dt)
+            with warnings.catch_warnings():
+                # read-only coefficient arrays: copied to the device, never written
+                warnings.simplefilter("ignore", UserWarning)
+                return torch.as_tensor(a, device=dev)
         self.vol_start = t(gt.vol_start)
         self.srow = t(gt.srow)
         self.shell_gid = t(gt.shell_gid)
