@@ -19,9 +19,8 @@ used purely as buffers.
 from __future__ import annotations
 
 import ctypes
-from functools import lru_cache
-
 import warnings
+from functools import lru_cache
 
 import numpy as np
 
