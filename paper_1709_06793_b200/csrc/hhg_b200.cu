@@ -505,19 +505,13 @@ int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s, const hhg_sur
   G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
   G.ent_col = gs->ent_col;
   G.ent_val = gs->ent_val;
-  if (s->nrows > 0) {
-    const int blocks = (int)((s->nrows + 127) / 128);
-    if (res) surface_csr_kernel<true><<<blocks, 128, 0, S(stream)>>>(G, out);
-    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out);
-    int rc = check("surface_csr_kernel");
-    if (rc) return rc;
-  }
-  if (s->ndir > 0) {
-    const int blocks = (int)((s->ndir + 255) / 256);
+  const long long total = s->nrows + s->ndir;   // surface rows, then Dirichlet rows
+  if (total > 0) {
+    const int blocks = (int)((total + 127) / 128);
     const long long *ids = reinterpret_cast<const long long *>(s->dir_ids);
-    if (res) dirichlet_kernel<true><<<blocks, 256, 0, S(stream)>>>(s->ndir, ids, u, out);
-    else dirichlet_kernel<false><<<blocks, 256, 0, S(stream)>>>(s->ndir, ids, u, out);
-    return check("dirichlet_kernel");
+    if (res) surface_csr_kernel<true><<<blocks, 128, 0, S(stream)>>>(G, out, s->ndir, ids);
+    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out, s->ndir, ids);
+    return check("surface_csr_kernel");
   }
   return HHG_OK;
 }

@@ -325,10 +325,19 @@ __device__ __forceinline__ void gs_surface_row_csr(const SurfGSDesc &G, long lon
 // surface_reduce_kernel, with w_d = (k0 + k_d) * psh_d (or the nodal s_d)
 // read instead of recomputed
 template <bool RES>
-__global__ void surface_csr_kernel(SurfGSDesc G, double *out) {
+__global__ void surface_csr_kernel(SurfGSDesc G, double *out, long long ndir,
+                                   const long long *dir_ids) {
   const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const SurfDesc &D = G.s;
-  if (r >= D.nrows) return;
+  if (r >= D.nrows) {
+    // Dirichlet rows ride along in the same launch: identity (0 for f - Au)
+    const long long e = r - D.nrows;
+    if (e < ndir) {
+      const long long g = dir_ids[e];
+      out[g] = RES ? 0.0 : D.u[g];
+    }
+    return;
+  }
   const long long gid = D.rows[r];
   const double v0 = D.u[gid];
   long long e = G.ent_ptr[r];
