@@ -361,7 +361,7 @@ class Operator:
                                         out.data_ptr(), st), "surface_apply")
 
     # -- host-buffer pipeline ---------------------------------------------------
-    def _pipeline(self, groups=16):
+    def _pipeline(self, groups=32):
         """Streams, events and per-group tile descriptors of apply_host."""
         if getattr(self, "_pipe", None) is None:
             import ctypes
