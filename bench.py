@@ -258,7 +258,7 @@ def run_own(args):
             "e2e": {"value": round(total_dofs / (e2e * 1e-3) / 1e9, 4), "unit": "GDoF/s",
                     "ms_per_step": round(e2e, 2), "h2d_bytes_per_step": 8 * grid.n_nodes,
                     "d2h_bytes_per_step": 8 * grid.n_nodes},
-            "gpu_launches": args.steps * 3,   # ghost, volume, surface+Dirichlet rows
+            "gpu_launches": args.steps * 4,   # ghost, volume, surface rows, Dirichlet rows
             "all_rows_gdofs": round(grid.n_nodes * world / (ms * 1e-3) / 1e9, 3),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

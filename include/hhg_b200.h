@@ -119,7 +119,8 @@ typedef struct hhg_grid {
   const double *kc;        /* [ntets*lat_size] coefficient, lattice layout   */
   const int32_t *tiles;    /* [ntiles*4] (tet, i0, j0, kmax) volume tiles    */
   int32_t ntiles;
-  int32_t pad_;
+  int32_t nmtiles;         /* tiles of the mirror (default scaling) kernel,  */
+  const int32_t *mtiles;   /* hhg_volume_tile_cols_mirror() columns wide     */
 } hhg_grid;
 
 typedef struct hhg_surface {
@@ -288,6 +289,8 @@ int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr,
 
 /* rows of one volume tile (W*B) the kernels were compiled with */
 int hhg_volume_tile_rows(void);
+/* columns of one tile of the mirror kernel (hhg_grid.mtiles) */
+int hhg_volume_tile_cols_mirror(void);
 
 /* status word of the last GS launch (HHG_OK / HHG_ERR_ZERO_DIAG) — call
  * after synchronising the stream */

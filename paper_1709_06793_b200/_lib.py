@@ -33,7 +33,7 @@ class HhgGrid(ctypes.Structure):
                 ("shell_size", ctypes.c_int64), ("n_nodes", ctypes.c_int64),
                 ("vol_start", vp), ("srow", vp), ("shell_gid", vp),
                 ("ghost", vp), ("kc", vp), ("tiles", vp),
-                ("ntiles", ctypes.c_int32), ("pad_", ctypes.c_int32)]
+                ("ntiles", ctypes.c_int32), ("nmtiles", ctypes.c_int32), ("mtiles", vp)]
 
 
 class HhgSurface(ctypes.Structure):
@@ -118,6 +118,7 @@ EXPORTS = {
     "hhg_status_reset": (ctypes.c_int, []),
     "hhg_build_info": (ctypes.c_char_p, []),
     "hhg_volume_tile_rows": (ctypes.c_int, []),
+    "hhg_volume_tile_cols_mirror": (ctypes.c_int, []),
     "hhg_host_gs_levels": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp]),
 }
 

@@ -74,23 +74,27 @@ static int launch_volume(const VolDesc &D, cudaStream_t st) {
   return check("volume_kernel");
 }
 
+#ifndef HHG_MIRROR_NW
+#define HHG_MIRROR_NW 4          // warps per CTA = tile columns / 8
+#endif
 #ifndef HHG_MIRROR_MINB
-#define HHG_MIRROR_MINB 2
+#define HHG_MIRROR_MINB (8 / HHG_MIRROR_NW)
 #endif
 
 template <int SRC, bool RES>
 static int launch_mirror(const VolDesc &D, cudaStream_t st) {
-  if (D.ntiles <= 0) return HHG_OK;
-  static_assert(kW == 4, "the mirror kernel uses 4 warps of 8x4 lanes");
-  constexpr int ROWS = kW * kB + 2;
-  const size_t smem = sizeof(double2) * kNS * ROWS * VOL_COLS;
-  auto kern = volume_kernel_mirror<SRC, RES, kB, kNS, HHG_MIRROR_MINB>;
+  if (D.nmtiles <= 0) return D.ntiles > 0 ? HHG_ERR_ARG : HHG_OK;
+  static_assert(kW == 4, "the mirror kernel uses 8x4-lane warps of 4B rows");
+  constexpr int NW = HHG_MIRROR_NW;
+  constexpr int ROWS = 4 * kB + 2;
+  const size_t smem = sizeof(double2) * kNS * ROWS * (8 * NW + 2);
+  auto kern = volume_kernel_mirror<SRC, RES, kB, kNS, HHG_MIRROR_MINB, NW>;
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     configured = true;
   }
-  kern<<<D.ntiles, 128, smem, st>>>(D);
+  kern<<<D.nmtiles, 32 * NW, smem, st>>>(D);
   return check("volume_kernel_mirror");
 }
 
@@ -369,6 +373,8 @@ static VolDesc grid_desc(const hhg_grid *g) {
   D.kc = g->kc;
   D.tiles = reinterpret_cast<const int4 *>(g->tiles);
   D.ntiles = g->ntiles;
+  D.mtiles = reinterpret_cast<const int4 *>(g->mtiles);
+  D.nmtiles = g->nmtiles;
   return D;
 }
 
@@ -505,13 +511,24 @@ int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s, const hhg_sur
   G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
   G.ent_col = gs->ent_col;
   G.ent_val = gs->ent_val;
-  const long long total = s->nrows + s->ndir;   // surface rows, then Dirichlet rows
+#ifndef HHG_FUSE_DIRICHLET
+#define HHG_FUSE_DIRICHLET 0
+#endif
+  const long long *ids = reinterpret_cast<const long long *>(s->dir_ids);
+  const long long nd = HHG_FUSE_DIRICHLET ? s->ndir : 0;
+  const long long total = s->nrows + nd;   // surface rows (then Dirichlet rows)
   if (total > 0) {
     const int blocks = (int)((total + 127) / 128);
-    const long long *ids = reinterpret_cast<const long long *>(s->dir_ids);
-    if (res) surface_csr_kernel<true><<<blocks, 128, 0, S(stream)>>>(G, out, s->ndir, ids);
-    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out, s->ndir, ids);
-    return check("surface_csr_kernel");
+    if (res) surface_csr_kernel<true><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids);
+    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids);
+    int rc = check("surface_csr_kernel");
+    if (rc) return rc;
+  }
+  if (!HHG_FUSE_DIRICHLET && s->ndir > 0) {
+    const int blocks = (int)((s->ndir + 255) / 256);
+    if (res) dirichlet_kernel<true><<<blocks, 256, 0, S(stream)>>>(s->ndir, ids, u, out);
+    else dirichlet_kernel<false><<<blocks, 256, 0, S(stream)>>>(s->ndir, ids, u, out);
+    return check("dirichlet_kernel");
   }
   return HHG_OK;
 }
@@ -787,6 +804,7 @@ int hhg_status_reset(void) {
 }
 
 int hhg_volume_tile_rows(void) { return kW * kB; }   // W*B rows (W/4 warp rows of 4B)
+int hhg_volume_tile_cols_mirror(void) { return 8 * HHG_MIRROR_NW; }
 
 // host-side level schedule of the surface Gauss-Seidel: rows are in
 // ascending global id, dep_idx[dep_ptr[r]..dep_ptr[r+1]) lists the row
@@ -810,8 +828,8 @@ int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr, const int64_t *dep
 
 const char *hhg_build_info(void) {
   static char buf[128];
-  snprintf(buf, sizeof buf, "sm_100a volume B=%d W=%d NS=%d MINB=%d", kB, kW, kNS,
-           HHG_VOL_MINB);
+  snprintf(buf, sizeof buf, "sm_100a volume B=%d W=%d NS=%d MINB=%d mirror NW=%d", kB, kW, kNS,
+           HHG_VOL_MINB, HHG_MIRROR_NW);
   return buf;
 }
 

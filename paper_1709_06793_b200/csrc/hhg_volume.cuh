@@ -40,6 +40,8 @@ struct VolDesc {
   const double *w;             // stored stencils [ntets*nvol*15]
   const int4 *tiles;
   int ntiles;
+  const int4 *mtiles;          // tiles of volume_kernel_mirror (8*NW columns)
+  int nmtiles;
 };
 
 enum VolSrc { SRC_SPLIT = 0, SRC_LATTICE = 1 };
@@ -182,15 +184,15 @@ struct Win {
   double2 L[B + 1];  // rows j0w   .. j0w+B
 };
 
-template <int B>
+template <int B, int COLS = VOL_COLS>
 __device__ __forceinline__ void load_win(Win<B> &w, const double2 *slot, int r0, int c) {
-  const double2 *base = slot + (r0 - 1) * VOL_COLS + c;
+  const double2 *base = slot + (r0 - 1) * COLS + c;
 #pragma unroll
-  for (int m = 0; m < B + 2; ++m) w.C[m] = base[m * VOL_COLS];
+  for (int m = 0; m < B + 2; ++m) w.C[m] = base[m * COLS];
 #pragma unroll
-  for (int m = 0; m < B + 1; ++m) w.R[m] = base[m * VOL_COLS + 1];
+  for (int m = 0; m < B + 1; ++m) w.R[m] = base[m * COLS + 1];
 #pragma unroll
-  for (int m = 0; m < B + 1; ++m) w.L[m] = base[(m + 1) * VOL_COLS - 1];
+  for (int m = 0; m < B + 1; ++m) w.L[m] = base[(m + 1) * COLS - 1];
 }
 
 // gather the 14 neighbours of output row s from below / mid / above windows
@@ -684,19 +686,21 @@ __device__ __forceinline__ void mirror_step(const Win<B> &mi, const Win<B> &hi,
   c.t5 = edge_term<B>(hi.C[B], mi.C[B + 1], sh[5]);
 }
 
-template <int SRC, bool RES, int B, int NS, int MINB>
-__global__ void __launch_bounds__(128, MINB)
+// NW warps per CTA, each 8 columns x 4B rows (8x4 lanes, B rows per lane):
+// a tile is 8*NW columns x 4B rows of one element, marching in k
+template <int SRC, bool RES, int B, int NS, int MINB, int NW>
+__global__ void __launch_bounds__(32 * NW, MINB)
 volume_kernel_mirror(VolDesc D) {
-  constexpr int W = 4;
-  constexpr int ROWS = W * B + 2;
-  constexpr int NT = 32 * W;
-  constexpr int NSLOT = (ROWS * VOL_COLS + NT - 1) / NT;
-  constexpr unsigned PLANE_BYTES = ROWS * VOL_COLS * sizeof(double2);
+  constexpr int ROWS = 4 * B + 2;
+  constexpr int COLS = 8 * NW + 2;
+  constexpr int NT = 32 * NW;
+  constexpr int NSLOT = (ROWS * COLS + NT - 1) / NT;
+  constexpr unsigned PLANE_BYTES = ROWS * COLS * sizeof(double2);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2 *ring = reinterpret_cast<double2 *>(smem_raw);
   const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(ring));
 
-  const int4 tile = D.tiles[blockIdx.x];
+  const int4 tile = D.mtiles[blockIdx.x];
   const int t = tile.x, i0 = tile.y, j0 = tile.z, kmax = tile.w;
   const int n = D.n;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -726,7 +730,7 @@ volume_kernel_mirror(VolDesc D) {
   if (threadIdx.x == 0) {
     for (int b = 0; b < NS; ++b) {
       mbar_init(full0 + 8 * b, NT);
-      mbar_init(empty0 + 8 * b, W);
+      mbar_init(empty0 + 8 * b, NW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -746,10 +750,10 @@ volume_kernel_mirror(VolDesc D) {
 #pragma unroll
   for (int m = 0; m < NSLOT; ++m) {
     const int e = threadIdx.x + m * NT;
-    const int r = e / VOL_COLS, cc = e - r * VOL_COLS;
+    const int r = e / COLS, cc = e - r * COLS;
     const int si = i0 - 1 + cc, sj = j0 - 1 + r;
     sl_[m].ij = si | (sj << 16);
-    sl_[m].pmax = (e < ROWS * VOL_COLS) ? n - si - sj : -1;
+    sl_[m].pmax = (e < ROWS * COLS) ? n - si - sj : -1;
     sl_[m].ko = sj * (n + 1) - sj * (sj - 1) / 2 + si;                   // plane 0
     sl_[m].vo = (sj - 1) * (n - 3) - (sj - 1) * (sj - 2) / 2 + si - 1;    // plane 1
     sl_[m].go = sl_[m].ko;                                               // plane 0
@@ -813,7 +817,7 @@ volume_kernel_mirror(VolDesc D) {
   auto fetch = [&](int q, Win<B> &w) {
     const int sl = q % NS;
     if (!full_ok) mbar_wait(full0 + 8 * sl, (q / NS) & 1);
-    load_win<B>(w, ring + sl * ROWS * VOL_COLS, r0, c);
+    load_win<B, COLS>(w, ring + sl * ROWS * COLS, r0, c);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sl);
 #if HHG_MBAR_PROBE

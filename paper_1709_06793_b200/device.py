@@ -68,7 +68,8 @@ def shell_layout(n: int):
 TILE_GROUP = 8   # macro elements whose j-bands are interleaved (L2 reuse)
 
 
-def volume_tiles(n: int, ntets: int, tile_rows: int, group: int = TILE_GROUP):
+def volume_tiles(n: int, ntets: int, tile_rows: int, group: int = TILE_GROUP,
+                 tile_cols: int = 32):
     """(tet, i0, j0, kmax) work tiles ordered by (element group, j-band,
     element, i): tiles sharing a halo column run back to back, and a band's
     halo rows are re-read by the next band of the same element while they
@@ -78,7 +79,7 @@ def volume_tiles(n: int, ntets: int, tile_rows: int, group: int = TILE_GROUP):
     for g0 in range(0, ntets, group):
         for j0 in range(1, n - 2, tile_rows):
             for t in range(g0, min(g0 + group, ntets)):
-                for i0 in range(1, n - 1 - j0, 32):
+                for i0 in range(1, n - 1 - j0, tile_cols):
                     tl.append((t, i0, j0, n - 1 - i0 - j0))
     if not tl:
         return np.zeros((0, 4), dtype=np.int32)
@@ -88,7 +89,7 @@ def volume_tiles(n: int, ntets: int, tile_rows: int, group: int = TILE_GROUP):
 class GridTables:
     """Host-side (numpy) tables of one grid level on one device."""
 
-    def __init__(self, grid, tile_rows=None):
+    def __init__(self, grid, tile_rows=None, mirror_cols=None):
         n = grid.n
         self.n = n
         self.ntets = grid.macro.n_elements
@@ -100,7 +101,12 @@ class GridTables:
         self.shell_gid = np.ascontiguousarray(grid.elem_gidx[:, self.shell_pos])
         if tile_rows is None:
             tile_rows = int(lib.hhg_volume_tile_rows())
+        if mirror_cols is None:
+            mirror_cols = int(lib.hhg_volume_tile_cols_mirror())
         self.tiles = volume_tiles(n, self.ntets, tile_rows)
+        # the default scaling kernel (volume_kernel_mirror) may use wider tiles
+        self.mtiles = self.tiles if mirror_cols == 32 else \
+            volume_tiles(n, self.ntets, tile_rows, tile_cols=mirror_cols)
 
 
 def _point_codes(lat, pos):
@@ -238,6 +244,7 @@ class DeviceGrid:
         self.ghost = torch.zeros(gt.ntets * gt.S, dtype=torch.float64, device=dev)
         self.kc = t(kc_values, np.float64).reshape(-1)
         self.tiles = t(gt.tiles)
+        self.mtiles = self.tiles if gt.mtiles is gt.tiles else t(gt.mtiles)
         d = HhgGrid()
         d.n, d.ntets = gt.n, gt.ntets
         d.lat_size, d.nvol, d.shell_size, d.n_nodes = gt.L, gt.nvol, gt.S, gt.n_nodes
@@ -248,6 +255,8 @@ class DeviceGrid:
         d.kc = self.kc.data_ptr()
         d.tiles = self.tiles.data_ptr() if len(gt.tiles) else None
         d.ntiles = len(gt.tiles)
+        d.mtiles = self.mtiles.data_ptr() if len(gt.mtiles) else None
+        d.nmtiles = len(gt.mtiles)
         self.desc = d
         self.ref = ctypes.byref(d)
 

@@ -371,16 +371,20 @@ class Operator:
             ne = grid.macro.n_elements
             ng = max(1, min(groups, ne))
             bounds = np.linspace(0, ne, ng + 1).astype(int)
-            tiles = dg.gt.tiles
+            tiles, mtiles = dg.gt.tiles, dg.gt.mtiles
             descs, keep = [], []
             for g in range(ng):
+                d = type(dg.desc).from_buffer_copy(dg.desc)
                 sel = (tiles[:, 0] >= bounds[g]) & (tiles[:, 0] < bounds[g + 1])
                 tg = torch.as_tensor(np.ascontiguousarray(tiles[sel]), device="cuda")
-                d = type(dg.desc).from_buffer_copy(dg.desc)
                 d.tiles = tg.data_ptr() if len(tg) else None
                 d.ntiles = int(sel.sum())
+                msel = (mtiles[:, 0] >= bounds[g]) & (mtiles[:, 0] < bounds[g + 1])
+                mg = torch.as_tensor(np.ascontiguousarray(mtiles[msel]), device="cuda")
+                d.mtiles = mg.data_ptr() if len(mg) else None
+                d.nmtiles = int(msel.sum())
                 descs.append(d)
-                keep.append(tg)
+                keep += [tg, mg]
             n = grid.n_nodes
             self._pipe = {
                 "bounds": bounds, "descs": descs, "keep": keep,

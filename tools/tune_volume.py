@@ -52,7 +52,7 @@ for B, W, NS, MINB, EXPT, EXTRA in configs:
         if hasattr(h, name):
             getattr(h, name).restype = res
             getattr(h, name).argtypes = args
-    gt = GridTables(grid, tile_rows=W * B)
+    gt = GridTables(grid, tile_rows=W * B, mirror_cols=int(h.hhg_volume_tile_cols_mirror()))
     dg = DeviceGrid(gt, kf.values)
     st = torch.cuda.current_stream().cuda_stream
     h.hhg_ghost_update(dg.ref, u.data_ptr(), st)
