@@ -283,3 +283,28 @@ def test_surface_modes_agree_bitwise(cuda, name):
     b = Operator(grid, v, kf, hybrid_nodal=hn, surface_mode="matrix-free")
     assert np.array_equal(a.apply(u), b.apply(u))
     assert np.array_equal(a.residual(u, f), b.residual(u, f))
+
+
+def test_surface_first_side_stream_path(cuda):
+    """The N > 1 path (ShardedOperator / bench.py): surface rows and the
+    interface hook on a side stream concurrently with the volume kernel must
+    give the same rows as the default order, for apply and residual."""
+    torch = cuda
+    grid = M.RefinedGrid(case_mesh("c3"), 4)
+    kf = sample_nodal(k_c3(), grid)
+    op = Operator(grid, "scaling", kf)
+    rng = np.random.default_rng(3)
+    u = torch.as_tensor(rng.uniform(-1, 1, grid.n_nodes), device="cuda")
+    f = torch.as_tensor(rng.uniform(-1, 1, grid.n_nodes), device="cuda")
+    calls = []
+
+    def hook(out):
+        calls.append(torch.cuda.current_stream().cuda_stream)
+        out.mul_(1.0)                      # a device op on the hook's stream
+    ref = op.apply_device(u).cpu().numpy()
+    got = op.apply_device(u, after_surface=hook).cpu().numpy()
+    assert np.array_equal(got, ref)
+    assert calls and calls[0] != torch.cuda.current_stream().cuda_stream
+    ref_r = op.apply_device(u, f=f).cpu().numpy()
+    got_r = op.apply_device(u, f=f, after_surface=hook).cpu().numpy()
+    assert np.array_equal(got_r, ref_r)
