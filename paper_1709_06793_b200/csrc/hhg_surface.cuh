@@ -7,8 +7,9 @@
 // reference stencil (only patch elements inside that macro element), so a
 // surface row is  sum_{incident elements} sum_d (k0+kq) psh_c[d] (vq - v0)
 // (scaling) or the nodal analogue with zeroed factors for outside elements.
-// One thread per row; incidences are visited in a fixed order, so results
-// are deterministic run to run.
+// Two passes (one thread per incidence, then one per row); incidences are
+// summed in a fixed order, so results are deterministic run to run.  The
+// default apply path precomputes these rows instead (hhg_smooth.cuh).
 #pragma once
 #include "hhg_common.cuh"
 
@@ -105,43 +106,6 @@ __device__ __forceinline__ void inc_gather(const SurfDesc &D, int t, int i, int 
   }
 }
 
-// MIXED = false: every row is a scaling row (no nodal factors on device)
-template <bool RES, bool MIXED>
-__global__ void __launch_bounds__(128)
-surface_kernel(SurfDesc D) {
-  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (r >= D.nrows) return;
-  const long long gid = D.rows[r];
-  const double v0 = D.u[gid];
-  const bool nodal = MIXED && D.row_nodal[r] != 0;
-  double row = 0.0;
-  for (int e = D.inc_ptr[r]; e < D.inc_ptr[r + 1]; ++e) {
-    const int t = D.inc_tet[e];
-    const int code = D.inc_code[e];
-    const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
-    const int cls = D.inc_cls[e];
-    const unsigned mask = c_cls_dirmask[cls];
-    double2 q[14];
-    double k0;
-    inc_gather(D, t, i, j, k, mask, v0, q, k0);
-    double part;
-    if (!MIXED || !nodal) {
-      const double *sh = D.psh + ((long long)t * 14 + cls) * 14;
-      part = 0.0;
-#pragma unroll
-      for (int d = 0; d < 14; ++d)
-        if (mask >> d & 1)
-          part = dadd(part, dmul(dmul(dadd(k0, q[d].y), __ldg(sh + d)), dsub(q[d].x, v0)));
-    } else {
-      const double *fac = D.pfac + ((long long)t * 14 + cls) * 72;
-      part = nodal_row_exact(v0, k0, q, fac);
-    }
-    row = dadd(row, part);
-  }
-  if (RES) row = dsub(D.f[gid], row);
-  D.out[gid] = row;
-}
-
 // pass 1: one thread per incidence in element-major (lattice) order — the
 // one-sided partial row of that boundary point; its own value comes from
 // the ghost shell, so neighbouring threads read neighbouring lattice points
@@ -179,7 +143,7 @@ surface_partial_kernel(SurfDesc D) {
 }
 
 // pass 2: one thread per free surface row, partials summed in element
-// order (identical association to the one-pass kernel above)
+// order (the association of surface_csr_kernel, hhg_smooth.cuh)
 template <bool RES>
 __global__ void surface_reduce_kernel(SurfDesc D) {
   const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
