@@ -470,12 +470,18 @@ class Operator:
         df, _ = self._to_dev(f, "right-hand side")
         return self._from_dev(self.apply_device(du, f=df), kind)
 
-    def smooth_device(self, du, df, sweeps=1, omega=1.0):
+    def smooth_device(self, du, df, sweeps=1, omega=1.0, check_diag=True):
         """Forward GS on device tensors.  Surface rows level by level, ghost
         refresh, then volume wavefronts.  const / stored smooth with the
         scaling (or, for a nodal source, nodal) sweep: their stencil weights
         are bitwise those rows ((c+c)*sh == (c*2)*sh; dumped weights are the
-        scaling/nodal row terms)."""
+        scaling/nodal row terms).
+
+        ``check_diag``: synchronise and raise the reference's "zero central
+        stencil entry" ValueError here (the public ``smooth``).  The
+        multigrid cycle passes False and checks the shared status word once
+        per solve, so a V-cycle enqueues its sweeps without host round
+        trips."""
         D = self._device()
         dg, ds = D["grid"], D["surf"]
         st = self._stream()
@@ -488,35 +494,34 @@ class Operator:
                 stack = self._fac if src == "nodal" else self._sh
                 coef = D["tcoef"] = D["torch"].as_tensor(
                     np.ascontiguousarray(np.stack(stack)), device="cuda").reshape(-1)
-            lib.hhg_status_reset()
-            for _ in range(sweeps):
-                check(lib.hhg_smooth_surface_all(dg.ref, ds.ref, gs["ref"], float(omega),
-                                                 du.data_ptr(), df.data_ptr(), st),
-                      "smooth_surface")
-                check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
+
+            def volume():
                 check(lib.hhg_tensor_smooth_volume(dg.ref, var, self.coeff.M,
                                                    D["km"].data_ptr(), coef.data_ptr(),
                                                    float(omega), du.data_ptr(),
                                                    df.data_ptr(),
                                                    self._lattice_work().data_ptr(), st),
                       "tensor_smooth_volume")
-            D["torch"].cuda.current_stream().synchronize()
-            check(lib.hhg_status(), "smooth")
-            return du
-        if src == "nodal":
-            var, coef = _lib.VAR["nodal"], D["coef"] if self._stored is None else D["fac"]
         else:
-            var, coef = _lib.VAR["scaling"], D["sh"]
-        lib.hhg_status_reset()
+            if src == "nodal":
+                var, coef = _lib.VAR["nodal"], D["coef"] if self._stored is None else D["fac"]
+            else:
+                var, coef = _lib.VAR["scaling"], D["sh"]
+
+            def volume():
+                check(lib.hhg_smooth_volume(dg.ref, var, coef.data_ptr(), float(omega),
+                                            du.data_ptr(), df.data_ptr(), st), "smooth_volume")
+        if check_diag:
+            lib.hhg_status_reset()
         for _ in range(sweeps):
             check(lib.hhg_smooth_surface_all(dg.ref, ds.ref, gs["ref"], float(omega),
                                              du.data_ptr(), df.data_ptr(), st),
                   "smooth_surface")
             check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
-            check(lib.hhg_smooth_volume(dg.ref, var, coef.data_ptr(), float(omega),
-                                        du.data_ptr(), df.data_ptr(), st), "smooth_volume")
-        D["torch"].cuda.current_stream().synchronize()
-        check(lib.hhg_status(), "smooth")
+            volume()
+        if check_diag:
+            D["torch"].cuda.current_stream().synchronize()
+            check(lib.hhg_status(), "smooth")
         return du
 
     def smooth(self, u, f, sweeps=1, omega=1.0):
