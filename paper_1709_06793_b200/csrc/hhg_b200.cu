@@ -624,9 +624,64 @@ static int ten_smem_ok() {
   return HHG_OK;
 }
 
+// tiles of the staged tensor kernel: (element, i0, j0, kmax), 32 x TR
+// points per plane, ordered (group of 8 elements, band, element, i) like the
+// scalar volume tiles so co-running CTAs share halo rows in L2
+struct TenTiles {
+  int n = -1, ntets = -1, tr = -1, count = 0;
+  int4 *dev = nullptr;
+};
+
+static int tensor_tiles(int n, int ntets, int tr, TenTiles &c) {
+  if (c.n == n && c.ntets == ntets && c.tr == tr) return HHG_OK;
+  std::vector<int4> tl;
+  for (int g0 = 0; g0 < ntets; g0 += 8)
+    for (int j0 = 1; j0 <= n - 3; j0 += tr)
+      for (int t = g0; t < std::min(g0 + 8, ntets); ++t)
+        for (int i0 = 1; i0 + j0 <= n - 2; i0 += 32) tl.push_back(make_int4(t, i0, j0, n - 1 - i0 - j0));
+  if (c.dev) cudaFree(c.dev);
+  c.dev = nullptr;
+  if (!tl.empty()) {
+    if (cudaMalloc(&c.dev, tl.size() * sizeof(int4)) != cudaSuccess) return HHG_ERR_CUDA;
+    cudaMemcpy(c.dev, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice);
+  }
+  c.n = n;
+  c.ntets = ntets;
+  c.tr = tr;
+  c.count = (int)tl.size();
+  return HHG_OK;
+}
+
+template <bool NODAL>
+static int ten_tile_apply(const TenDesc &D, bool res, cudaStream_t st) {
+  static TenTiles cache;
+  static bool configured = false;
+  int rc = tensor_tiles(D.n, D.ntets, tt_rows<NODAL>(), cache);
+  if (rc) return rc;
+  const int smem = (int)tt_smem<NODAL>();
+  if (!configured) {
+    if (cudaFuncSetAttribute(tensor_tile_kernel<NODAL, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ||
+        cudaFuncSetAttribute(tensor_tile_kernel<NODAL, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
+      return HHG_ERR_CUDA;
+    configured = true;
+  }
+  if (cache.count == 0) return HHG_OK;
+  if (res)
+    tensor_tile_kernel<NODAL, true><<<cache.count, tt_threads<NODAL>(), smem, st>>>(D, cache.dev);
+  else
+    tensor_tile_kernel<NODAL, false><<<cache.count, tt_threads<NODAL>(), smem, st>>>(D, cache.dev);
+  return check("tensor_tile_kernel");
+}
+
 template <bool NODAL, bool AOS>
 static int ten_apply(const TenDesc &D, bool res, cudaStream_t st) {
   if (D.n < 4) return HHG_OK;
+#ifndef HHG_TENSOR_TILED
+#define HHG_TENSOR_TILED 1
+#endif
+  if (AOS && HHG_TENSOR_TILED) return ten_tile_apply<NODAL>(D, res, st);
   int rc = ten_smem_ok<NODAL, AOS>();
   if (rc) return rc;
   constexpr int R = ten_rows<NODAL>();

@@ -20,6 +20,7 @@
 #include "hhg_common.cuh"
 #include "hhg_smooth.cuh"
 #include "hhg_surface.cuh"
+#include "hhg_volume.cuh"
 
 namespace hhg {
 
@@ -210,6 +211,171 @@ tensor_volume_kernel(TenDesc D) {
     ten_row<NODAL, false, AOS>(D, P, i, j, ut, kt, sc, es, tid, NT, acc, diag, v0);
     ot[c0 + i] = RES ? dsub(ft[c0 + i], acc) : acc;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Staged apply: a CTA owns a tile of 32 columns (i) x TR rows (j) of one
+// element and marches the planes k upward.  Every plane of the tile plus a
+// one-point halo (34 x (TR+2) points: value + 48-byte component record) is
+// copied into a 4-slot shared-memory ring with cp.async, two planes ahead;
+// each thread then forms one row of plane k from slots k-1, k, k+1.  Same
+// arithmetic and order as ten_row (bitwise equal), but the 15 neighbour
+// records come from shared memory instead of 15 scattered L1/L2 requests.
+// ---------------------------------------------------------------------------
+constexpr int kTenCols = 34;     // 32 + halo
+constexpr int kTenNS = 4;        // ring slots (planes k-1, k, k+1, k+2)
+
+template <bool NODAL>
+constexpr int tt_rows() { return NODAL ? 2 : 4; }   // tile rows (j)
+template <bool NODAL>
+constexpr int tt_per() { return NODAL ? 1 : 2; }    // rows per thread
+template <bool NODAL>
+constexpr int tt_threads() { return 32 * tt_rows<NODAL>() / tt_per<NODAL>(); }
+template <bool NODAL>
+constexpr size_t tt_smem() {
+  return sizeof(double) * ((size_t)kTenNS * (tt_rows<NODAL>() + 2) * kTenCols * (1 + kTenM) +
+                           kTenM * ten_ncoef<NODAL>() +
+                           (NODAL ? (size_t)kTenM * 24 * tt_threads<NODAL>() : 0));
+}
+
+template <bool NODAL, bool RES>
+__global__ void __launch_bounds__(tt_threads<NODAL>())
+tensor_tile_kernel(TenDesc D, const int4 *tiles) {
+  constexpr int TR = tt_rows<NODAL>();
+  constexpr int P = tt_per<NODAL>();
+  constexpr int NT = tt_threads<NODAL>();
+  constexpr int PTS = (TR + 2) * kTenCols;        // staged points per plane
+  constexpr int NC = ten_ncoef<NODAL>();
+  extern __shared__ __align__(16) double tt_sm[];
+  double *sv = tt_sm;                              // [NS][PTS] values
+  double *sk = sv + kTenNS * PTS;                  // [NS][PTS][M] records
+  double *sc = sk + kTenNS * PTS * kTenM;          // coefficients
+  double *es = sc + kTenM * NC;                    // nodal element sums
+  const int4 tile = tiles[blockIdx.x];
+  const int t = tile.x, i0 = tile.y, j0 = tile.z, kmax = tile.w;
+  const int n = D.n;
+  const int tid = threadIdx.x, lane = tid & 31, wr = tid >> 5;
+  for (int e = tid; e < kTenM * NC; e += NT) sc[e] = D.coef[(long long)t * kTenM * NC + e];
+  const double *ut = D.u + (long long)t * D.L;
+  const double *kt = D.km + (long long)t * kTenM * D.L;
+
+  auto stage = [&](int p) {
+    if (p <= n) {
+      const int slot = p % kTenNS;
+      const int tn = n - p;                        // plane p is a size-(n-p) triangle
+      const int pb = tetra32(n) - tetra32(n - p);  // lattice offset of plane p
+#pragma unroll
+      for (int r = 0; r < (PTS + NT - 1) / NT; ++r) {
+        const int e = tid + r * NT;
+        if (e < PTS) {
+          const int rr = e / kTenCols, cc = e - rr * kTenCols;
+          const int si = i0 - 1 + cc, sj = j0 - 1 + rr;
+          if (si >= 0 && sj >= 0 && si + sj <= tn) {
+            const int off = pb + sj * (tn + 1) - sj * (sj - 1) / 2 + si;
+            cp_async8(sv + slot * PTS + e, ut + off);
+            const double *src = kt + (long long)kTenM * off;
+            double *dst = sk + ((long long)slot * PTS + e) * kTenM;
+#pragma unroll
+            for (int h = 0; h < kTenM / 2; ++h) {
+              const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst + 2 * h));
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d),
+                           "l"(src + 2 * h));
+            }
+          }
+        }
+      }
+    }
+    cp_async_commit();
+  };
+
+  stage(0);
+  stage(1);
+  stage(2);
+  const int i = i0 + lane;
+  const int lx = lane + 1;
+  const long long o0 = D.out_split ? D.vol_start[t] : (long long)t * D.nvol;
+  double *ot = D.out + o0;
+  const double *ft = RES ? D.f + o0 : nullptr;
+  const int m4 = n - 4;
+  for (int k = 1; k <= kmax; ++k) {
+    stage(k + 2);
+    cp_async_wait<1>();                            // planes <= k + 1 have landed
+    __syncthreads();
+    const int s0 = ((k - 1) % kTenNS) * PTS, s1 = (k % kTenNS) * PTS,
+              s2 = ((k + 1) % kTenNS) * PTS;
+    // this thread's rows j = j0 + wr + q * (TR / P), q < P
+    bool live[P];
+    int pc[P];
+    int po[P][14];
+    double v0[P], acc[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      const int ly = wr + q * (TR / P) + 1;
+      live[q] = i + (j0 + ly - 1) + k <= n - 1;
+      pc[q] = s1 + ly * kTenCols + lx;
+      v0[q] = sv[pc[q]];
+#pragma unroll
+      for (int d = 0; d < 14; ++d) {
+        const int dk = c_dirs_h(d, 2);
+        const int sb = dk < 0 ? s0 : (dk > 0 ? s2 : s1);
+        po[q][d] = sb + (ly + c_dirs_h(d, 1)) * kTenCols + lx + c_dirs_h(d, 0);
+      }
+    }
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < P; ++q) any |= live[q];
+    if (any) {
+      if constexpr (!NODAL) {
+        double k0[P][kTenM];
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+#pragma unroll
+          for (int m = 0; m < kTenM; ++m) k0[q][m] = sk[pc[q] * kTenM + m];
+#pragma unroll
+        for (int d = 0; d < 14; ++d) {
+          double cd[kTenM];                        // component weights of d, shared by the rows
+#pragma unroll
+          for (int m = 0; m < kTenM; ++m) cd[m] = sc[m * 14 + d];
+#pragma unroll
+          for (int q = 0; q < P; ++q) {
+            const double *kq = sk + po[q][d] * kTenM;
+            double s = dmul(dadd(k0[q][0], kq[0]), cd[0]);
+#pragma unroll
+            for (int m = 1; m < kTenM; ++m) s = dadd(s, dmul(dadd(k0[q][m], kq[m]), cd[m]));
+            const double term = dmul(s, dsub(sv[po[q][d]], v0[q]));
+            acc[q] = d == 0 ? term : dadd(acc[q], term);
+          }
+        }
+      } else {
+        // P == 1
+#pragma unroll 1
+        for (int m = 0; m < kTenM; ++m) {
+          double b[55];
+          b[0] = sk[pc[0] * kTenM + m];
+#pragma unroll
+          for (int d = 0; d < 14; ++d) b[1 + d] = sk[po[0][d] * kTenM + m];
+          cse_steps<0>(b);
+#pragma unroll
+          for (int e = 0; e < 24; ++e) es[(m * 24 + e) * NT + tid] = b[31 + e];
+        }
+        double vq[14], diag = 0.0;
+#pragma unroll
+        for (int d = 0; d < 14; ++d) vq[d] = sv[po[0][d]];
+        ten_nodal_acc<0, false>(acc[0], diag, vq, v0[0], es, NT, tid, sc);
+      }
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+        if (live[q]) {
+          const int j = j0 + wr + q * (TR / P);
+          // volume rank of (i, j, k): inner-lattice row (k-1, j-1) + i - 1
+          const int c = tetra32(m4) - tetra32(m4 - (k - 1)) + (j - 1) * (n - 2 - k) -
+                        (j - 1) * (j - 2) / 2 + i - 1;
+          ot[c] = RES ? dsub(ft[c], acc[q]) : acc[q];
+        }
+    }
+    __syncthreads();                               // slot (k-1) % NS is refilled next
+  }
+  cp_async_wait<0>();
 }
 
 // forward Gauss-Seidel on the lattice arrays: one CTA per element walks
