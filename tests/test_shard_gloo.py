@@ -60,12 +60,13 @@ def _worker(rank, world, port, level, variant, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("variant", ["scaling", "nodal"])
-def test_two_rank_slabs_equal_single_domain(variant):
+@pytest.mark.parametrize("variant,world", [("scaling", 2), ("nodal", 2), ("scaling", 3)])
+def test_two_rank_slabs_equal_single_domain(variant, world):
+    """world 3: the middle rank exchanges with both neighbours."""
     from oracle.assemble import CpuOperator
     from paper_1709_06793_b200.coefficients import sample_nodal
     from paper_1709_06793_b200.mesh import RefinedGrid, kuhn_blocks
-    world, level = 2, 3
+    level = 3
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -78,7 +79,8 @@ def test_two_rank_slabs_equal_single_domain(variant):
         p.join(timeout=60)
         assert p.exitcode == 0
 
-    gmesh = kuhn_blocks(np.linspace(0, 1, 3), np.linspace(0, 1, 3), np.array([0.0, 0.5, 1.0]))
+    gmesh = kuhn_blocks(np.linspace(0, 1, 3), np.linspace(0, 1, 3),
+                        0.5 * np.arange(world + 1, dtype=float))
     grid = RefinedGrid(gmesh, level)
     op = CpuOperator(grid, variant, sample_nodal(_kfun, grid))
     u = _ufun(grid.node_coords)
@@ -88,13 +90,15 @@ def test_two_rank_slabs_equal_single_domain(variant):
     for rank, X, out, _, _ in res:
         gids = np.array([index[tuple(x)] for x in X])
         assert np.abs(out - ref[gids]).max() <= 1e-13 * scale
-    # interface rows bitwise identical on both ranks
-    (_, X0, o0, d0, n0), (_, X1, o1, d1, n1) = res
-    assert np.array_equal(o0[n0[1]], o1[n1[0]])
-    assert np.array_equal(X0[n0[1]], X1[n1[0]])
-    # owner-masked dot == single-domain dot
-    assert d0 == d1
-    assert abs(d0 - float(ref @ u)) <= 1e-12 * abs(float(ref @ u)) + 1e-12
+    # interface rows bitwise identical on both sides of every interface
+    for a, b in zip(res[:-1], res[1:]):
+        (ra, Xa, oa, da, na), (rb, Xb, ob, db, nb) = a, b
+        assert np.array_equal(oa[na[rb]], ob[nb[ra]])
+        assert np.array_equal(Xa[na[rb]], Xb[nb[ra]])
+    # owner-masked dot == single-domain dot, the same on every rank
+    dots = [r[3] for r in res]
+    assert all(d == dots[0] for d in dots)
+    assert abs(dots[0] - float(ref @ u)) <= 1e-12 * abs(float(ref @ u)) + 1e-12
 
 
 def _cg_worker(rank, world, port, level, q):
