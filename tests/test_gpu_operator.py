@@ -308,3 +308,38 @@ def test_surface_first_side_stream_path(cuda):
     ref_r = op.apply_device(u, f=f).cpu().numpy()
     got_r = op.apply_device(u, f=f, after_surface=hook).cpu().numpy()
     assert np.array_equal(got_r, ref_r)
+
+
+@pytest.mark.slow
+def test_config5_full_size(cuda):
+    """BASELINE config 5 at its full per-GPU size (96 macro elements, level 8,
+    2.7e8 unknowns): constants are annihilated exactly on free rows, three
+    elements' volume rows are bitwise the C oracle's, and the operator is
+    linear and symmetric on the free nodes."""
+    from tests.cases import k_c5
+    torch = cuda
+    grid = M.RefinedGrid(case_mesh("c5"), 8)
+    kf = sample_nodal(k_c5(), grid)
+    op = Operator(grid, "scaling", kf)
+    free = torch.as_tensor(~grid.dirichlet_mask, device="cuda")
+    ones = torch.ones(grid.n_nodes, dtype=torch.float64, device="cuda")
+    assert torch.where(free, op.apply(ones), 0).abs().max().item() == 0.0
+    rng = np.random.default_rng(5)
+    u = rng.uniform(-1, 1, grid.n_nodes)
+    du = torch.as_tensor(u, device="cuda")
+    out = op.apply(du)
+    nvol = grid.nodes_per_volume
+    for t in (0, 47, 95):
+        want = ok.apply_scaling_3d(grid.n, grid.lat.base, u[grid.elem_gidx[t]], kf.values[t],
+                                   op._sh[t])
+        s0 = int(grid.vol_start[t])
+        assert np.array_equal(out[s0:s0 + nvol].cpu().numpy(), want), t
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    y = torch.rand(grid.n_nodes, dtype=torch.float64, device="cuda", generator=gen) * free
+    x = du * free
+    Ax, Ay = op.apply(x), op.apply(y)
+    Axy = op.apply(2.0 * x - 3.0 * y)
+    assert (Axy - (2.0 * Ax - 3.0 * Ay)).abs().max().item() <= 1e-12 * Ax.abs().max().item()
+    s1 = torch.dot(y, Ax * free).item()
+    s2 = torch.dot(x, Ay * free).item()
+    assert abs(s1 - s2) <= 1e-10 * abs(s1)
