@@ -70,25 +70,6 @@ __device__ __forceinline__ void mbar_arrive(unsigned bar) {
 __device__ __forceinline__ void mbar_arrive_cp_async(unsigned bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
-#ifndef HHG_MBAR_PROBE
-#define HHG_MBAR_PROBE 0
-#endif
-#ifndef HHG_LATE_REFILL
-#define HHG_LATE_REFILL 0
-#endif
-// non-blocking probe: the result is consumed a step later, so the
-// ~150-cycle phase check overlaps the arithmetic instead of stalling
-__device__ __forceinline__ unsigned mbar_test(unsigned bar, unsigned parity) {
-  unsigned ok;
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      " mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-      " selp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(bar), "r"(parity)
-      : "memory");
-  return ok;
-}
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -601,57 +582,11 @@ __device__ __forceinline__ void mirror_seed(const Win<B> &lo, const Win<B> &mi,
 
 // rows of plane kk from windows mi (kk) and hi (kk+1) plus the carry;
 // leaves the carry for plane kk+1.  Accumulation order d = 0..13 exactly.
-#ifndef HHG_MIRROR_INTERLEAVE
-#define HHG_MIRROR_INTERLEAVE 0
-#endif
 template <int B>
 __device__ __forceinline__ void mirror_step(const Win<B> &mi, const Win<B> &hi,
                                             const double (&sh)[7], MirrorCarry<B> &c,
                                             double (&out)[B]) {
   double t1[B], n2[B], n12[B];
-#if HHG_MIRROR_INTERLEAVE
-  // direction-major: the B rows' terms of one direction side by side
-  double a[B];
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = edge_term<B>(mi.C[s + 1], mi.R[s + 1], sh[0]);      // d 0
-#pragma unroll
-  for (int s = 0; s < B; ++s) {
-    t1[s] = edge_term<B>(mi.C[s + 1], mi.C[s + 2], sh[1]);                             // d 1
-    a[s] = dadd(a[s], t1[s]);
-  }
-#pragma unroll
-  for (int s = 0; s < B; ++s) {
-    n2[s] = edge_term<B>(mi.C[s + 1], hi.C[s + 1], sh[2]);                             // d 2
-    a[s] = dadd(a[s], n2[s]);
-  }
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], mi.R[s], sh[3]));  // d 3
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], c.t4[s]);                              // d 4
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = (s + 1 < B) ? dsub(a[s], c.t12[s + 1]) : dadd(a[s], c.t5);  // d 5
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], hi.R[s], sh[6]));  // d 6
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], mi.L[s], sh[0]));  // d 7
-#pragma unroll
-  for (int s = 0; s < B; ++s)
-    a[s] = (s >= 1) ? dsub(a[s], t1[s - 1])
-                    : dadd(a[s], edge_term<B>(mi.C[s + 1], mi.C[s], sh[1]));            // d 8
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = dsub(a[s], c.t2[s]);                              // d 9
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], mi.L[s + 1], sh[3]));  // d 10
-#pragma unroll
-  for (int s = 0; s < B; ++s) a[s] = dadd(a[s], edge_term<B>(mi.C[s + 1], hi.L[s], sh[4]));  // d 11
-#pragma unroll
-  for (int s = 0; s < B; ++s) {
-    n12[s] = edge_term<B>(mi.C[s + 1], hi.C[s], sh[5]);                                // d 12
-    a[s] = dadd(a[s], n12[s]);
-  }
-#pragma unroll
-  for (int s = 0; s < B; ++s) out[s] = dadd(a[s], c.t13[s]);                           // d 13
-#else
 #pragma unroll
   for (int s = 0; s < B; ++s) {
     const double2 p = mi.C[s + 1];
@@ -675,7 +610,6 @@ __device__ __forceinline__ void mirror_step(const Win<B> &mi, const Win<B> &hi,
     a = dadd(a, c.t13[s]);                                          // d 13
     out[s] = a;
   }
-#endif
 #pragma unroll
   for (int s = 0; s < B; ++s) {
     c.t2[s] = n2[s];
@@ -759,9 +693,9 @@ volume_kernel_mirror(VolDesc D) {
     sl_[m].go = sl_[m].ko;                                               // plane 0
   }
   const int t2n = (n + 1) * (n + 2) / 2;
-  auto produce = [&](int p, unsigned empty_ok) {
+  auto produce = [&](int p) {
     const int sl = p % NS;
-    if (p >= NS && !empty_ok) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
+    if (p >= NS) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
     const unsigned off = ring_s + (unsigned)sl * PLANE_BYTES;
     const bool copy = HHG_VOL_EXPT != 2 || p < PD;   // EXPT 2: arithmetic only
 #pragma unroll
@@ -792,7 +726,7 @@ volume_kernel_mirror(VolDesc D) {
     mbar_arrive_cp_async(full0 + 8 * sl);
   };
 
-  for (int p = 0; p < PD && p <= kmax + 1; ++p) produce(p, 0u);
+  for (int p = 0; p < PD && p <= kmax + 1; ++p) produce(p);
 
   const int li = lane & 7, lj = lane >> 3;
   const int r0 = 1 + lj * B;
@@ -811,27 +745,14 @@ volume_kernel_mirror(VolDesc D) {
   Win<B> X0, X1, X2;
   MirrorCarry<B> carry;
 
-  // fetch plane q into window w and release its slot; then probe (without
-  // blocking) the barriers the next step and this step's producer need
-  unsigned full_ok = 0u, empty_ok = 0u;
+  // fetch plane q into window w, release its slot, refill PD planes ahead
   auto fetch = [&](int q, Win<B> &w) {
     const int sl = q % NS;
-    if (!full_ok) mbar_wait(full0 + 8 * sl, (q / NS) & 1);
+    mbar_wait(full0 + 8 * sl, (q / NS) & 1);
     load_win<B, COLS>(w, ring + sl * ROWS * COLS, r0, c);
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sl);
-#if HHG_MBAR_PROBE
-    const int q1 = q + 1;
-    full_ok = q1 <= kmax + 1 ? mbar_test(full0 + 8 * (q1 % NS), (q1 / NS) & 1) : 1u;
-#endif
-#if HHG_LATE_REFILL == 0
-    if (q + PD <= kmax + 1) produce(q + PD, 0u);
-#endif
-  };
-  auto refill = [&](int q) {
-#if HHG_LATE_REFILL
-    if (q + PD <= kmax + 1) produce(q + PD, empty_ok);
-#endif
+    if (q + PD <= kmax + 1) produce(q + PD);
   };
   auto emit = [&](int kk, const double (&vals)[B]) {
     const int lim = n - 1 - kk;
@@ -859,14 +780,11 @@ volume_kernel_mirror(VolDesc D) {
       }
       emit(q - 1, vals);
     }
-    refill(q);
   };
 
   if (kmax >= 1) {
     fetch(0, X0);
-    refill(0);
     fetch(1, X1);
-    refill(1);
     if (warp_min_ij <= n - 2) mirror_seed<B>(X0, X1, sh, carry);
     step(2, X1, X2);
     for (int q = 3; q <= kmax + 1; q += 3) {
