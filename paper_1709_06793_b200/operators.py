@@ -414,6 +414,8 @@ class Operator:
         nv = grid.nodes_per_volume
         flags = self._vol_flags()
         wp = D["w"].data_ptr() if D["w"] is not None else None
+        if self.surface_mode == "csr":
+            ds.csr(dg)          # one-time fill on this stream, before the others join it
         cur = torch.cuda.current_stream()
         for st in P["streams"]:
             st.wait_stream(cur)

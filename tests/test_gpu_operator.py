@@ -343,3 +343,23 @@ def test_config5_full_size(cuda):
     s1 = torch.dot(y, Ax * free).item()
     s2 = torch.dot(x, Ay * free).item()
     assert abs(s1 - s2) <= 1e-10 * abs(s1)
+
+
+@pytest.mark.parametrize("name", ["scaling", "nodal", "const", "hybrid:wv+we", "stored"])
+def test_pinned_host_pipeline_equals_device_apply(cuda, name):
+    """Operator.apply on a pinned CPU tensor runs the overlapped H2D /
+    per-group volume kernels / D2H pipeline (the bench's e2e path); it must
+    return exactly the device-resident apply."""
+    torch = cuda
+    grid = M.RefinedGrid(case_mesh("c3"), 4)
+    kf = sample_nodal(k_c3(), grid)
+    op = _op(grid, kf, "scaling" if name == "stored" else name)
+    if name == "stored":
+        op = op.store_stencils()
+    u = np.random.default_rng(21).uniform(-1, 1, grid.n_nodes)
+    host = torch.from_numpy(u).pin_memory()
+    got = op.apply(host)
+    assert got.device.type == "cpu" and got.is_pinned()
+    want = op.apply_device(torch.as_tensor(u, device="cuda")).cpu().numpy()
+    assert np.array_equal(got.numpy(), want)
+    assert np.array_equal(op.apply(u), want)           # numpy in, numpy out
