@@ -5,6 +5,8 @@
 #include <stdio.h>
 
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <vector>
 
 #include "../../include/hhg_b200.h"
@@ -142,30 +144,40 @@ static std::vector<int4> make_tiles(int n, int ntets) {
   return tl;
 }
 
-// per-element ABI: one macro element, lattice layout (tiles cached per n)
+// Small host-built tables (tile lists, hyperplane point lists) are uploaded
+// once per parameter set and kept for the process lifetime: never freed, so
+// kernels queued earlier on any stream can still read them (a multigrid
+// cycle alternates levels, so a single-entry cache would rebuild and free
+// a table per sweep).
+template <class T>
+static int upload(const std::vector<T> &v, T **dev) {
+  *dev = nullptr;
+  if (v.empty()) return HHG_OK;
+  if (cudaMalloc(dev, v.size() * sizeof(T)) != cudaSuccess) return HHG_ERR_CUDA;
+  return cudaMemcpy(*dev, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice) == cudaSuccess
+             ? HHG_OK
+             : HHG_ERR_CUDA;
+}
+
+// per-element ABI: one macro element, lattice layout (tiles per n)
 struct ElemTiles {
-  int n = -1;
   int4 *dev = nullptr;
   int count = 0;
 };
-static ElemTiles g_elem_tiles;
 
 static int elem_tiles(int n, const int4 **tiles, int *count) {
-  if (g_elem_tiles.n != n) {
+  static std::map<int, ElemTiles> cache;
+  auto it = cache.find(n);
+  if (it == cache.end()) {
     std::vector<int4> tl = make_tiles(n, 1);
-    if (g_elem_tiles.dev) cudaFree(g_elem_tiles.dev);
-    g_elem_tiles.dev = nullptr;
-    if (!tl.empty()) {
-      if (cudaMalloc(&g_elem_tiles.dev, tl.size() * sizeof(int4)) != cudaSuccess)
-        return HHG_ERR_CUDA;
-      cudaMemcpy(g_elem_tiles.dev, tl.data(), tl.size() * sizeof(int4),
-                 cudaMemcpyHostToDevice);
-    }
-    g_elem_tiles.n = n;
-    g_elem_tiles.count = (int)tl.size();
+    ElemTiles e;
+    int rc = upload(tl, &e.dev);
+    if (rc) return rc;
+    e.count = (int)tl.size();
+    it = cache.emplace(n, e).first;
   }
-  *tiles = g_elem_tiles.dev;
-  *count = g_elem_tiles.count;
+  *tiles = it->second.dev;
+  *count = it->second.count;
   return HHG_OK;
 }
 
@@ -286,15 +298,15 @@ int hhg_apply_stored_3d(int64_t n, const int64_t *, const double *v, const doubl
 
 // interior points of each hyperplane h = i + 2j + 3k (host-built once per n)
 struct Hyperplanes {
-  int n = -1;
   int *ptr = nullptr, *code = nullptr;
 };
-static Hyperplanes g_hp;
 
 static int hyperplanes(int n, const int **ptr, const int **code) {
-  if (g_hp.n != n) {
+  static std::map<int, Hyperplanes> cache;
+  auto it = cache.find(n);
+  if (it == cache.end()) {
     const int hmin = 6, hmax = 3 * n - 6;
-    std::vector<int> p(hmax - hmin + 2, 0), c;
+    std::vector<int> p(std::max(hmax - hmin + 2, 1), 0), c;
     for (int h = hmin; h <= hmax; ++h) {
       p[h - hmin] = (int)c.size();
       for (int k = 1; k <= n - 3; ++k)
@@ -303,19 +315,15 @@ static int hyperplanes(int n, const int **ptr, const int **code) {
           if (i >= 1 && i + j + k <= n - 1) c.push_back(i | (j << 10) | (k << 20));
         }
     }
-    p[hmax - hmin + 1] = (int)c.size();
-    if (g_hp.ptr) cudaFree(g_hp.ptr);
-    if (g_hp.code) cudaFree(g_hp.code);
-    if (cudaMalloc(&g_hp.ptr, p.size() * sizeof(int)) != cudaSuccess) return HHG_ERR_CUDA;
-    if (cudaMalloc(&g_hp.code, std::max<size_t>(c.size(), 1) * sizeof(int)) != cudaSuccess)
-      return HHG_ERR_CUDA;
-    cudaMemcpy(g_hp.ptr, p.data(), p.size() * sizeof(int), cudaMemcpyHostToDevice);
-    if (!c.empty())
-      cudaMemcpy(g_hp.code, c.data(), c.size() * sizeof(int), cudaMemcpyHostToDevice);
-    g_hp.n = n;
+    if (hmax >= hmin) p[hmax - hmin + 1] = (int)c.size();
+    Hyperplanes hp;
+    int rc = upload(p, &hp.ptr);
+    if (!rc) rc = upload(c, &hp.code);
+    if (rc) return rc;
+    it = cache.emplace(n, hp).first;
   }
-  *ptr = g_hp.ptr;
-  *code = g_hp.code;
+  *ptr = it->second.ptr;
+  *code = it->second.code;
   return HHG_OK;
 }
 
@@ -628,33 +636,34 @@ static int ten_smem_ok() {
 // points per plane, ordered (group of 8 elements, band, element, i) like the
 // scalar volume tiles so co-running CTAs share halo rows in L2
 struct TenTiles {
-  int n = -1, ntets = -1, tr = -1, count = 0;
+  int count = 0;
   int4 *dev = nullptr;
 };
 
-static int tensor_tiles(int n, int ntets, int tr, TenTiles &c) {
-  if (c.n == n && c.ntets == ntets && c.tr == tr) return HHG_OK;
-  std::vector<int4> tl;
-  for (int g0 = 0; g0 < ntets; g0 += 8)
-    for (int j0 = 1; j0 <= n - 3; j0 += tr)
-      for (int t = g0; t < std::min(g0 + 8, ntets); ++t)
-        for (int i0 = 1; i0 + j0 <= n - 2; i0 += 32) tl.push_back(make_int4(t, i0, j0, n - 1 - i0 - j0));
-  if (c.dev) cudaFree(c.dev);
-  c.dev = nullptr;
-  if (!tl.empty()) {
-    if (cudaMalloc(&c.dev, tl.size() * sizeof(int4)) != cudaSuccess) return HHG_ERR_CUDA;
-    cudaMemcpy(c.dev, tl.data(), tl.size() * sizeof(int4), cudaMemcpyHostToDevice);
+static int tensor_tiles(int n, int ntets, int tr, TenTiles &out) {
+  static std::map<std::tuple<int, int, int>, TenTiles> cache;
+  const auto key = std::make_tuple(n, ntets, tr);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    std::vector<int4> tl;
+    for (int g0 = 0; g0 < ntets; g0 += 8)
+      for (int j0 = 1; j0 <= n - 3; j0 += tr)
+        for (int t = g0; t < std::min(g0 + 8, ntets); ++t)
+          for (int i0 = 1; i0 + j0 <= n - 2; i0 += 32)
+            tl.push_back(make_int4(t, i0, j0, n - 1 - i0 - j0));
+    TenTiles e;
+    int rc = upload(tl, &e.dev);
+    if (rc) return rc;
+    e.count = (int)tl.size();
+    it = cache.emplace(key, e).first;
   }
-  c.n = n;
-  c.ntets = ntets;
-  c.tr = tr;
-  c.count = (int)tl.size();
+  out = it->second;
   return HHG_OK;
 }
 
 template <bool NODAL>
 static int ten_tile_apply(const TenDesc &D, bool res, cudaStream_t st) {
-  static TenTiles cache;
+  TenTiles cache;
   static bool configured = false;
   int rc = tensor_tiles(D.n, D.ntets, tt_rows<NODAL>(), cache);
   if (rc) return rc;
