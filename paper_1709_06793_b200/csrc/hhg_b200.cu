@@ -90,6 +90,19 @@ static int launch_mirror(const VolDesc &D, cudaStream_t st) {
   constexpr int NW = HHG_MIRROR_NW;
   constexpr int ROWS = 4 * kB + 2;
   const size_t smem = sizeof(double2) * kNS * ROWS * (8 * NW + 2);
+#ifndef HHG_VOLUME_WS
+#define HHG_VOLUME_WS 0          // warp-specialised producer / consumer form
+#endif
+  if (HHG_VOLUME_WS && NW == 4) {
+    auto kern = volume_kernel_ws<SRC, RES, kB, kNS>;
+    static bool configured_ws = false;
+    if (!configured_ws) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configured_ws = true;
+    }
+    kern<<<D.nmtiles, 256, smem, st>>>(D);
+    return check("volume_kernel_ws");
+  }
   auto kern = volume_kernel_mirror<SRC, RES, kB, kNS, HHG_MIRROR_MINB, NW>;
   static bool configured = false;
   if (!configured) {

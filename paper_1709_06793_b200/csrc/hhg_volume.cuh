@@ -798,4 +798,174 @@ volume_kernel_mirror(VolDesc D) {
   cp_async_wait<0>();
 }
 
+
+// ---------------------------------------------------------------------------
+// Warp-specialised form of volume_kernel_mirror: one warpgroup of producers
+// (128 threads, 4 staging slots each, setmaxnreg 40) fills the plane ring
+// with cp.async and runs up to NS planes ahead, bounded only by the empty
+// barriers; one warpgroup of consumers (setmaxnreg 216) does window loads,
+// the mirror arithmetic and the stores, with no staging instructions in its
+// stream.  Same tiles, ring, lane layout and arithmetic as the mirror kernel
+// (bitwise equal).  2 CTAs x 8 warps per SM.
+// ---------------------------------------------------------------------------
+template <int SRC, bool RES, int B, int NS>
+__global__ void __launch_bounds__(256, 2)
+volume_kernel_ws(VolDesc D) {
+  constexpr int NW = 4;                     // consumer warps (8 columns each)
+  constexpr int ROWS = 4 * B + 2;
+  constexpr int COLS = 8 * NW + 2;
+  constexpr int NP = 128;                   // producer threads
+  constexpr int NSLOT = (ROWS * COLS + NP - 1) / NP;
+  constexpr unsigned PLANE_BYTES = ROWS * COLS * sizeof(double2);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2 *ring = reinterpret_cast<double2 *>(smem_raw);
+  const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(ring));
+
+  const int4 tile = D.mtiles[blockIdx.x];
+  const int t = tile.x, i0 = tile.y, j0 = tile.z, kmax = tile.w;
+  const int n = D.n;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  __shared__ __align__(8) unsigned long long bars[2 * NS];
+  const unsigned full0 = static_cast<unsigned>(__cvta_generic_to_shared(&bars[0]));
+  const unsigned empty0 = full0 + NS * 8;
+  if (threadIdx.x == 0) {
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(full0 + 8 * b, NP);
+      mbar_init(empty0 + 8 * b, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp >= NW) {
+    // ---------------- producer warpgroup ----------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+    const int ptid = threadIdx.x - NW * 32;
+    const double *Tk = opaque(D.kc + (long long)t * D.L);
+    const double *Tv, *Tg;
+    if (SRC == SRC_SPLIT) {
+      Tv = opaque(D.u + D.vol_start[t]);
+      Tg = opaque(D.ghost + (long long)t * D.S);
+    } else {
+      Tv = opaque(D.u + (long long)t * D.L);
+      Tg = nullptr;
+    }
+    int ko[NSLOT], vo[NSLOT], go[NSLOT], pmax[NSLOT], ij[NSLOT];
+#pragma unroll
+    for (int m = 0; m < NSLOT; ++m) {
+      const int e = ptid + m * NP;
+      const int r = e / COLS, cc = e - r * COLS;
+      const int si = i0 - 1 + cc, sj = j0 - 1 + r;
+      ij[m] = si | (sj << 16);
+      pmax[m] = (e < ROWS * COLS) ? n - si - sj : -1;
+      ko[m] = sj * (n + 1) - sj * (sj - 1) / 2 + si;                   // plane 0
+      vo[m] = (sj - 1) * (n - 3) - (sj - 1) * (sj - 2) / 2 + si - 1;    // plane 1
+      go[m] = ko[m];                                                   // plane 0
+    }
+    const int t2n = (n + 1) * (n + 2) / 2;
+    for (int p = 0; p <= kmax + 1; ++p) {
+      const int sl = p % NS;
+      if (p >= NS) mbar_wait(empty0 + 8 * sl, ((p / NS) - 1) & 1);
+      const unsigned off = ring_s + (unsigned)sl * PLANE_BYTES;
+#pragma unroll
+      for (int m = 0; m < NSLOT; ++m) {
+        const int si = ij[m] & 0xffff, sj = ij[m] >> 16;
+        const int live = p <= pmax[m];
+        const bool interior = p >= 1 && si >= 1 && sj >= 1 && p < pmax[m];
+        const double *vs = interior ? at(Tv, vo[m]) : at(Tg, go[m]);
+        const double *ks = at(Tk, ko[m]);
+        const unsigned d = off + (unsigned)(ptid + m * NP) * sizeof(double2);
+        asm volatile(
+            "{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n"
+            " @q cp.async.ca.shared.global [%0], [%1], 8;\n"
+            " @q cp.async.ca.shared.global [%2], [%3], 8;\n}\n" ::"r"(d),
+            "l"(vs), "r"(d + 8), "l"(ks), "r"(live));
+        ko[m] += (n - p + 1) * (n - p) / 2 + (n - p + 1) - sj;
+        if (p >= 1) vo[m] += (n - 2 - p) * (n - 1 - p) / 2 - (sj - 1);
+        if (p == 0)
+          go[m] = t2n + (sj == 0 ? si : n + 2 * (sj - 1) + (si > 0 ? 1 : 0));
+        else
+          go[m] += 3 * (n - p) - (sj > 0 ? 1 : 0);
+      }
+      mbar_arrive_cp_async(full0 + 8 * sl);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  // ---------------- consumer warpgroup ----------------
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 216;\n" ::: "memory");
+  double *To, *Tf;
+  if (SRC == SRC_SPLIT) {
+    const long long vs = D.vol_start[t];
+    To = opaque(D.out + vs);
+    Tf = RES ? opaque(const_cast<double *>(D.f) + vs) : nullptr;
+  } else {
+    To = opaque(D.out + (long long)t * D.nvol);
+    Tf = RES ? opaque(const_cast<double *>(D.f) + (long long)t * D.nvol) : nullptr;
+  }
+  double sh[7];
+#pragma unroll
+  for (int d = 0; d < 7; ++d) sh[d] = __ldg(D.coef + (long long)t * D.coef_stride + d);
+
+  const int li = lane & 7, lj = lane >> 3;
+  const int r0 = 1 + lj * B;
+  const int c = 1 + warp * 8 + li;
+  const int i = i0 + warp * 8 + li;
+  const int jw = j0 + lj * B;
+  const int warp_min_ij = i0 + warp * 8 + j0;
+  const int m4 = n - 4;
+  int oterm[B];
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const int jj = jw + s - 1;
+    oterm[s] = -jj * (jj - 1) / 2 + i - 1;
+  }
+
+  Win<B> X0, X1, X2;
+  MirrorCarry<B> carry;
+  auto fetch = [&](int q, Win<B> &w) {
+    const int sl = q % NS;
+    mbar_wait(full0 + 8 * sl, (q / NS) & 1);
+    load_win<B, COLS>(w, ring + sl * ROWS * COLS, r0, c);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty0 + 8 * sl);
+  };
+  auto emit = [&](int kk, const double (&vals)[B]) {
+    const int lim = n - 1 - kk;
+    const int iplane = tetra32(m4) - tetra32(m4 - (kk - 1));
+    const int rowi = m4 + 2 - kk;
+#pragma unroll
+    for (int s = 0; s < B; ++s)
+      if (i + jw + s <= lim) {
+        const int cidx = iplane + (jw + s - 1) * rowi + oterm[s];
+        double val = vals[s];
+        if (RES) val = dsub(__ldg(at(Tf, cidx)), val);
+        __stcs(at(To, cidx), val);
+      }
+  };
+  auto step = [&](int q, Win<B> &mi, Win<B> &hi) {
+    fetch(q, hi);
+    if (warp_min_ij <= n - q) {
+      double vals[B];
+      mirror_step<B>(mi, hi, sh, carry, vals);
+      emit(q - 1, vals);
+    }
+  };
+  if (kmax >= 1) {
+    fetch(0, X0);
+    fetch(1, X1);
+    if (warp_min_ij <= n - 2) mirror_seed<B>(X0, X1, sh, carry);
+    step(2, X1, X2);
+    for (int q = 3; q <= kmax + 1; q += 3) {
+      step(q, X2, X0);
+      if (q + 1 > kmax + 1) break;
+      step(q + 1, X0, X1);
+      if (q + 2 > kmax + 1) break;
+      step(q + 2, X1, X2);
+    }
+  }
+}
+
 }  // namespace hhg
