@@ -30,6 +30,9 @@ import itertools
 from enum import IntEnum
 from functools import lru_cache
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 
 __all__ = [
@@ -53,6 +56,18 @@ LOCAL_EDGES_3D = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
 # face f is opposite local vertex f
 LOCAL_FACES_3D = ((1, 2, 3), (0, 2, 3), (0, 1, 3), (0, 1, 2))
 
+
+
+def _parallel(fn, count):
+    """fn(0..count-1) on a thread pool (per-element numpy work on disjoint
+    slices: same values as the serial loop)."""
+    workers = min(count, os.cpu_count() or 1, 16)
+    if workers <= 1 or count < 4:
+        for i in range(count):
+            fn(i)
+        return
+    with ThreadPoolExecutor(max_workers=workers) as ex:
+        list(ex.map(fn, range(count)))
 
 class PrimitiveKind(IntEnum):
     VERTEX = 0
@@ -474,11 +489,22 @@ class RefinedGrid:
                 X[s:s + npf] = V[a] + st[:, :1] / n * (V[b] - V[a]) \
                     + st[:, 1:] / n * (V[c] - V[a])
         if npv:
-            ijk = SimplexLattice(3, n - 4).coords + 1
-            for t_, conn in enumerate(m.elements):
+            # cast once: int64 @ float64 casts the lattice to float64 on
+            # every call before the same float matmul (identical values)
+            ijk = (SimplexLattice(3, n - 4).coords + 1).astype(np.float64)
+
+            def element(t_):
+                # V0 + (ijk @ E) / n evaluated in place (same operations)
+                conn = m.elements[t_]
                 s = self.vol_start[t_]
                 E = V[conn[1:]] - V[conn[0]]
-                X[s:s + npv] = V[conn[0]] + (ijk @ E) / n
+                dst = X[s:s + npv]
+                np.matmul(ijk, E, out=dst)
+                np.divide(dst, n, out=dst)
+                np.add(V[conn[0]], dst, out=dst)
+
+            # elements are independent slices; numpy releases the GIL
+            _parallel(element, m.n_elements)
         self.node_coords = X
 
     # -- per-element lattice -> global id -----------------------------------
