@@ -352,9 +352,23 @@ def sec_tensor():
     save("tensor_mg", f=f, residuals=np.array(rep.residuals), u=u)
 
 
+def sec_coeff():
+    """Coefficient sampling and the k_min safeguard field of the reference."""
+    from hhgscale.coefficients import kmin_field as r_kmin
+    out = {}
+    for tag, mesh, lvl, kfn in [("cube6_l3", M.unit_cube_6(), 3, wiggle3d),
+                                ("kuhn48_l2", case_mesh("c3"), 2, k_c3()),
+                                ("simplex_l4", M.reference_simplex(3), 4, k_c1())]:
+        g = RM.RefinedGrid(rmesh(mesh), lvl)
+        kf = r_sample(kfn, g)
+        out[f"{tag}_values"] = kf.values
+        out[f"{tag}_kmin"] = r_kmin(kf).values
+    save("coeff", **out)
+
+
 SECTIONS = {"mesh": sec_mesh, "kernels": sec_kernels, "applies": sec_applies,
             "c3": sec_c3_checksums, "c2": sec_c2_cg, "mg": sec_mg_small, "c4": sec_c4_mg,
-            "tensor": sec_tensor}
+            "tensor": sec_tensor, "coeff": sec_coeff}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(SECTIONS)):

@@ -107,3 +107,22 @@ def test_generators():
     assert c5.n_elements == 96
     g = M.RefinedGrid(M.unit_cube_12(), 0)
     assert (~g.dirichlet_mask).sum() == 1      # one interior macro vertex
+
+
+@pytest.mark.parametrize("tag,make,lvl,kname", [
+    ("cube6_l3", "unit_cube_6", 3, "wiggle"),
+    ("kuhn48_l2", "c3", 2, "c3"),
+    ("simplex_l4", "simplex", 4, "c1")])
+def test_coefficient_sampling_and_kmin_bitwise(tag, make, lvl, kname):
+    """sample_nodal and kmin_field (coefficients.py:47-92) reproduce the
+    reference's lattice arrays bit for bit."""
+    from paper_1709_06793_b200.coefficients import kmin_field, sample_nodal
+    from tests.cases import case_mesh, k_c1, k_c3, wiggle3d
+    g = golden("coeff")
+    mesh = {"unit_cube_6": M.unit_cube_6, "c3": lambda: case_mesh("c3"),
+            "simplex": lambda: M.reference_simplex(3)}[make]()
+    kfn = {"wiggle": wiggle3d, "c3": k_c3(), "c1": k_c1()}[kname]
+    grid = M.RefinedGrid(mesh, lvl)
+    kf = sample_nodal(kfn, grid)
+    assert np.array_equal(kf.values, g[f"{tag}_values"])
+    assert np.array_equal(kmin_field(kf).values, g[f"{tag}_kmin"])
