@@ -136,3 +136,20 @@ def test_mg_preconditioned_cg_config4_like(cuda):
     assert np.linalg.norm(r) <= 1.05e-8 * np.linalg.norm(r0)
     assert rep.iterations < rep_mg.iterations
     assert rep.residuals[-1] <= 1e-8 * rep.residuals[0]
+
+
+@pytest.mark.parametrize("variant", ["scaling", "nodal"])
+def test_vcycle_fixed_point(cuda, variant):
+    """The discrete solution is a fixed point of the V-cycle (the reference's
+    tests/test_multigrid.py:184-197 property): with f = A u*, one cycle from
+    u* changes it by at most 1e-12."""
+    hier = GridHierarchy(M.unit_cube_6(), 4, variant, cos3d(3))
+    grid = hier.grids[4]
+    op = hier.ops[4]
+    rng = np.random.default_rng(11)
+    ustar = rng.uniform(-1, 1, grid.n_nodes)
+    ustar[grid.dirichlet_mask] = 0.0
+    f = op.apply(ustar)
+    u = ustar.copy()
+    vcycle(hier, u, f, pre=2, post=2)
+    assert np.abs(u - ustar).max() <= 1e-12 * np.abs(ustar).max()
