@@ -363,3 +363,17 @@ def test_pinned_host_pipeline_equals_device_apply(cuda, name):
     want = op.apply_device(torch.as_tensor(u, device="cuda")).cpu().numpy()
     assert np.array_equal(got.numpy(), want)
     assert np.array_equal(op.apply(u), want)           # numpy in, numpy out
+
+
+def test_constant_field_collapses_variants(cuda):
+    """k = const makes scaling, nodal and scaling_ma2 the constant-coefficient
+    operator (the reference's tests/test_oracle.py:37-43, in 3-D)."""
+    grid = M.RefinedGrid(M.unit_cube_6(), 4)
+    cval = 2.5
+    kf = sample_nodal(lambda x: np.full(len(x), cval), grid)
+    u = np.random.default_rng(8).normal(size=grid.n_nodes)
+    ref = Operator(grid, "const", cval).apply(u)
+    scale = np.abs(ref).max()
+    for variant in ("scaling", "nodal", "scaling_ma2"):
+        out = Operator(grid, variant, kf).apply(u)
+        assert np.abs(out - ref).max() <= 1e-13 * scale, variant
