@@ -19,7 +19,7 @@ from .operators import VARIANTS, Operator, parse_hybrid_set
 __version__ = "0.1.0"
 
 __all__ = [
-    "CoefficientField", "catalog", "kmin_field", "sample_nodal",
+    "CoefficientField", "TensorCoefficient", "catalog", "kmin_field", "sample_nodal",
     "analytic_count", "traffic", "DIRS_3D", "MacroMesh", "PrimitiveKind",
     "RefinedGrid", "SimplexLattice", "cylinder_shell_box", "kuhn_blocks",
     "lattice_elements", "load_macro_mesh", "reference_simplex",
