@@ -764,7 +764,11 @@ volume_kernel_mirror(VolDesc D) {
         const int cidx = iplane + (jw + s - 1) * rowi + oterm[s];
         double val = vals[s];
         if (RES) val = dsub(__ldg(at(T.f, cidx)), val);
-        __stcs(at(T.o, cidx), val);
+        if (HHG_VOL_EXPT == 3) {                 // ablation: no stores
+          if (val == 12345.678) __stcs(at(T.o, cidx), val);
+        } else {
+          __stcs(at(T.o, cidx), val);
+        }
       }
   };
   // output plane kk = q - 1 from mi (plane kk) and hi (plane kk + 1)
