@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--fast", action="store_true",
                     help="FMA / mirror-pair arithmetic (default: bitwise reference order)")
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1 interface exchange: peer-memory push fused into the "
+                         "surface-row kernel (CUDA IPC over NVLink) or NCCL send/recv")
     ap.add_argument("--cpu-tets", type=int, default=16,
                     help="macro elements per CPU-baseline step (bounded sample)")
     return ap.parse_args()
@@ -148,7 +151,7 @@ def run_own(args):
     if imap is not None:
         from paper_1709_06793_b200.shard import ShardedOperator
         idx_t = {k: torch.as_tensor(v, device="cuda") for k, v in imap.neighbours.items()}
-        sop = ShardedOperator(op, imap, dist, grid.dirichlet_mask)
+        sop = ShardedOperator(op, imap, dist, grid.dirichlet_mask, transport=args.exchange)
     torch.cuda.synchronize()
     t_setup = time.time() - t_setup
 
@@ -163,6 +166,9 @@ def run_own(args):
         if record:
             ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             vol_ev.append(ev)
+        if sop is not None and sop.peer is not None:
+            sop.peer.apply(du, out=out, volume_events=ev)
+            return
         hook = None
         if imap is not None:
             hook = lambda o: exchange_partials(o, imap, dist, idx_t)  # noqa: E731

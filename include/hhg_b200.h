@@ -217,6 +217,39 @@ int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s,
                           const hhg_surface_gs *gs, int flags, const double *u,
                           const double *f, double *out, void *stream);
 
+/* ---------------------------------------------------------------------
+ * multi-GPU interface exchange over peer memory (one process per GPU,
+ * SURVEY.md §8e).  The interface rows' one-sided values are pushed into the
+ * neighbour's receive buffer by the kernel that computes them, a signal
+ * bumps the neighbour's arrival counter, and a pull kernel completes the
+ * rows in rank order once the neighbour's values have arrived.
+ * --------------------------------------------------------------------- */
+
+/* apply (no residual) surface + Dirichlet rows as hhg_surface_apply_csr,
+ * and for rows r with push_slot[r] >= 0 also store the row's value into
+ * dst0[push_slot[r]] (slot < split) or dst1[push_slot[r] - split]: peer
+ * device pointers (CUDA IPC) of the neighbours' receive buffers */
+int hhg_surface_apply_csr_push(const hhg_grid *g, const hhg_surface *s,
+                               const hhg_surface_gs *gs, const double *u, double *out,
+                               const int32_t *push_slot, double *dst0, double *dst1,
+                               int64_t split, void *stream);
+/* system-scope fence, then atomically add 1 to the neighbour's counter */
+int hhg_p2p_signal(unsigned long long *remote_flag, void *stream);
+/* wait (bounded; *err = 1 on timeout) until *flag >= target, then
+ * out[ids[i]] = recv_first ? recv[i] + out[ids[i]] : out[ids[i]] + recv[i] */
+int hhg_p2p_pull(double *out, const int64_t *ids, int64_t count, const double *recv,
+                 const unsigned long long *flag, unsigned long long target,
+                 int recv_first, int *err, void *stream);
+/* zero-initialised device allocation of its own (an IPC handle maps a whole
+ * allocation, so exchange buffers are not sub-allocated) / release */
+int hhg_device_alloc(int64_t bytes, void **ptr);
+int hhg_device_free(void *ptr);
+/* CUDA IPC plumbing: 64-byte handle of a hhg_device_alloc allocation; open /
+ * close a peer's allocation in this process */
+int hhg_ipc_get_handle(const void *ptr, void *handle);
+int hhg_ipc_open_handle(const void *handle, void **ptr);
+int hhg_ipc_close_handle(void *ptr);
+
 int hhg_smooth_surface_prepare(const hhg_grid *g, const hhg_surface *s,
                                const hhg_surface_gs *gs, void *stream);
 /* every level of the surface sweep in one cooperative launch */

@@ -107,6 +107,18 @@ EXPORTS = {
                                                   ctypes.POINTER(HhgSurface),
                                                   ctypes.POINTER(HhgSurfaceGS), ctypes.c_int,
                                                   vp, vp]),
+    "hhg_surface_apply_csr_push": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                                  ctypes.POINTER(HhgSurface),
+                                                  ctypes.POINTER(HhgSurfaceGS), vp, vp, vp,
+                                                  vp, vp, ctypes.c_int64, vp]),
+    "hhg_p2p_signal": (ctypes.c_int, [vp, vp]),
+    "hhg_p2p_pull": (ctypes.c_int, [vp, vp, ctypes.c_int64, vp, vp, ctypes.c_uint64,
+                                    ctypes.c_int, vp, vp]),
+    "hhg_device_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "hhg_device_free": (ctypes.c_int, [vp]),
+    "hhg_ipc_get_handle": (ctypes.c_int, [vp, vp]),
+    "hhg_ipc_open_handle": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_void_p)]),
+    "hhg_ipc_close_handle": (ctypes.c_int, [vp]),
     "hhg_dot": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),
     "hhg_axpy_ratio": (ctypes.c_int, [ctypes.c_int64, vp, vp, ctypes.c_double, vp,
                                       vp, vp]),

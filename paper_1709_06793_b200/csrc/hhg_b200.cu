@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <string.h>
 
 #include <algorithm>
 #include <map>
@@ -520,9 +521,74 @@ int hhg_smooth_surface_prepare(const hhg_grid *g, const hhg_surface *s,
 }
 
 // surface rows of apply / residual from the precomputed rows (+ Dirichlet)
+static int surface_csr(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
+                       int flags, const double *u, const double *f, double *out,
+                       const SurfPush &push, void *stream);
+
 int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
                           int flags, const double *u, const double *f, double *out,
                           void *stream) {
+  return surface_csr(g, s, gs, flags, u, f, out, SurfPush{}, stream);
+}
+
+int hhg_surface_apply_csr_push(const hhg_grid *g, const hhg_surface *s,
+                               const hhg_surface_gs *gs, const double *u, double *out,
+                               const int32_t *push_slot, double *dst0, double *dst1,
+                               int64_t split, void *stream) {
+  if (!push_slot) return HHG_ERR_ARG;
+  SurfPush p{push_slot, dst0, dst1, (long long)split};
+  return surface_csr(g, s, gs, 0, u, nullptr, out, p, stream);
+}
+
+int hhg_p2p_signal(unsigned long long *remote_flag, void *stream) {
+  if (!remote_flag) return HHG_ERR_ARG;
+  p2p_signal_kernel<<<1, 1, 0, S(stream)>>>(remote_flag);
+  return check("p2p_signal_kernel");
+}
+
+int hhg_p2p_pull(double *out, const int64_t *ids, int64_t count, const double *recv,
+                 const unsigned long long *flag, unsigned long long target, int recv_first,
+                 int *err, void *stream) {
+  if (count <= 0) return HHG_OK;
+  if (!out || !ids || !recv || !flag || !err) return HHG_ERR_ARG;
+  const int blocks = (int)std::min<int64_t>((count + 255) / 256, 64);
+  p2p_pull_kernel<<<blocks, 256, 0, S(stream)>>>(out, reinterpret_cast<const long long *>(ids),
+                                                count, recv, flag, target, recv_first, err);
+  return check("p2p_pull_kernel");
+}
+
+int hhg_device_alloc(int64_t bytes, void **ptr) {
+  if (bytes <= 0 || !ptr) return HHG_ERR_ARG;
+  if (cudaMalloc(ptr, (size_t)bytes) != cudaSuccess) return HHG_ERR_CUDA;
+  return cudaMemset(*ptr, 0, (size_t)bytes) == cudaSuccess ? HHG_OK : HHG_ERR_CUDA;
+}
+
+int hhg_device_free(void *ptr) { return cudaFree(ptr) == cudaSuccess ? HHG_OK : HHG_ERR_CUDA; }
+
+int hhg_ipc_get_handle(const void *ptr, void *handle) {
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void *>(ptr)) != cudaSuccess) return HHG_ERR_CUDA;
+  memcpy(handle, &h, sizeof h);
+  return HHG_OK;
+}
+
+int hhg_ipc_open_handle(const void *handle, void **ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  return cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess
+             ? HHG_OK
+             : HHG_ERR_CUDA;
+}
+
+int hhg_ipc_close_handle(void *ptr) {
+  return cudaIpcCloseMemHandle(ptr) == cudaSuccess ? HHG_OK : HHG_ERR_CUDA;
+}
+
+}  // extern "C"
+
+static int surface_csr(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
+                       int flags, const double *u, const double *f, double *out,
+                       const SurfPush &push, void *stream) {
   if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   const bool res = flags & HHG_FLAG_RESIDUAL;
   SurfGSDesc G{};
@@ -541,7 +607,7 @@ int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s, const hhg_sur
   if (total > 0) {
     const int blocks = (int)((total + 127) / 128);
     if (res) surface_csr_kernel<true><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids);
-    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids);
+    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids, push);
     int rc = check("surface_csr_kernel");
     if (rc) return rc;
   }
@@ -553,6 +619,8 @@ int hhg_surface_apply_csr(const hhg_grid *g, const hhg_surface *s, const hhg_sur
   }
   return HHG_OK;
 }
+
+extern "C" {
 
 // every level of the surface sweep in one cooperative launch; the grid is
 // sized to the mean level width (a narrow sweep syncs few blocks)

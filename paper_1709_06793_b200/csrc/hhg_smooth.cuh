@@ -324,9 +324,20 @@ __device__ __forceinline__ void gs_surface_row_csr(const SurfGSDesc &G, long lon
 // parts (incidence order) — the association of surface_partial_kernel +
 // surface_reduce_kernel, with w_d = (k0 + k_d) * psh_d (or the nodal s_d)
 // read instead of recomputed
+// Interface push (multi-GPU, peer memory): rows with push_slot[r] >= 0 are
+// interface rows shared with a neighbour rank; their one-sided value is
+// also stored straight into that neighbour's receive buffer over NVLink
+// (dst0 for slots < split, dst1 otherwise), in the same kernel that
+// computes it.
+struct SurfPush {
+  const int *slot;      // [nrows] or nullptr
+  double *dst0, *dst1;  // peer receive buffers (this apply's parity)
+  long long split;
+};
+
 template <bool RES>
 __global__ void surface_csr_kernel(SurfGSDesc G, double *out, long long ndir,
-                                   const long long *dir_ids) {
+                                   const long long *dir_ids, SurfPush push = SurfPush{}) {
   const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const SurfDesc &D = G.s;
   if (r >= D.nrows) {
@@ -364,6 +375,52 @@ __global__ void surface_csr_kernel(SurfGSDesc G, double *out, long long ndir,
   }
   if (RES) row = dsub(D.f[gid], row);
   out[gid] = row;
+  if (!RES && push.slot) {
+    const int sl = __ldg(push.slot + r);
+    if (sl >= 0) {
+      if (sl < push.split) push.dst0[sl] = row;
+      else push.dst1[sl - push.split] = row;
+    }
+  }
+}
+
+// after the pushes of this apply: make them visible system-wide, then bump
+// the neighbour's arrival counter (one signal per apply and neighbour)
+__global__ void p2p_signal_kernel(unsigned long long *remote_flag) {
+  __threadfence_system();
+  atomicAdd_system(remote_flag, 1ULL);
+}
+
+// wait until the neighbour's push of this apply has arrived (its counter
+// reaches `target`; bounded spin, *err set on timeout), then complete the
+// interface rows in rank order: out = recv + mine if recv_first else
+// mine + recv (bitwise the NCCL path's sum on both ranks)
+__global__ void p2p_pull_kernel(double *out, const long long *ids, long long count,
+                                const double *recv, const unsigned long long *flag,
+                                unsigned long long target, int recv_first, int *err) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    unsigned long long v = 0;
+    long long spins = 0;
+    for (;;) {
+      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+      if (v >= target) break;
+      if (++spins > (1LL << 30)) break;          // ~a minute: never hang the GPU
+      __nanosleep(64);
+    }
+    ok = v >= target;
+    if (!ok) atomicExch(err, 1);
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  }
+  __syncthreads();
+  if (!ok) return;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long g = ids[i];
+    const double theirs = __ldcv(recv + i);
+    const double mine = out[g];
+    out[g] = recv_first ? dadd(theirs, mine) : dadd(mine, theirs);
+  }
 }
 
 __global__ void gs_surface_kernel(SurfGSDesc G) {

@@ -289,7 +289,8 @@ class Operator:
     def _stream(self):
         return self._device()["torch"].cuda.current_stream().cuda_stream
 
-    def apply_device(self, du, out=None, f=None, after_surface=None, volume_events=None):
+    def apply_device(self, du, out=None, f=None, after_surface=None, volume_events=None,
+                     push=None):
         """Device-resident A u (or f - A u when f is given), torch tensors.
 
         Order: ghost update, volume rows, surface + Dirichlet rows.  With
@@ -321,11 +322,11 @@ class Operator:
                 side = D["side"] = torch.cuda.Stream()
             side.wait_stream(main)
             with torch.cuda.stream(side):
-                self._surface(dg, ds, res, du, fp, out, side.cuda_stream)
+                self._surface(dg, ds, res, du, fp, out, side.cuda_stream, push=push)
                 if after_surface is not None:
                     after_surface(out)
         if not concurrent and after_surface is not None:
-            self._surface(dg, ds, res, du, fp, out, st)
+            self._surface(dg, ds, res, du, fp, out, st, push=push)
             after_surface(out)
         if volume_events is not None:
             volume_events[0].record(main)
@@ -345,15 +346,22 @@ class Operator:
         if concurrent:
             main.wait_stream(side)
         elif after_surface is None:
-            self._surface(dg, ds, res, du, fp, out, st)
+            self._surface(dg, ds, res, du, fp, out, st, push=push)
         self._count()
         return out
 
-    def _surface(self, dg, ds, res_flag, du, fp, out, st):
+    def _surface(self, dg, ds, res_flag, du, fp, out, st, push=None):
         """Surface + Dirichlet rows: from the precomputed rows when built
-        (setup on first use, `surface_mode="csr"`), else matrix-free."""
+        (setup on first use, `surface_mode="csr"`), else matrix-free.
+        ``push`` = (slot_ptr, dst0, dst1, split): also store the interface
+        rows into the neighbours' receive buffers (shard.PeerExchange)."""
         if self.surface_mode == "csr":
             c = ds.csr(dg)
+            if push is not None and not res_flag:
+                check(lib.hhg_surface_apply_csr_push(dg.ref, ds.ref, c["ref"], du.data_ptr(),
+                                                     out.data_ptr(), *push, st),
+                      "surface_apply_csr_push")
+                return
             check(lib.hhg_surface_apply_csr(dg.ref, ds.ref, c["ref"], res_flag, du.data_ptr(),
                                             fp, out.data_ptr(), st), "surface_apply_csr")
         else:

@@ -25,7 +25,7 @@ import numpy as np
 from .mesh import MacroMesh, kuhn_blocks
 
 __all__ = ["slab_mesh", "InterfaceMap", "exchange_partials", "owned_mask",
-           "ShardedOperator", "sharded_cg"]
+           "ShardedOperator", "sharded_cg", "PeerExchange"]
 
 
 def slab_mesh(rank: int, world: int, nx: int = 4, ny: int = 4) -> MacroMesh:
@@ -107,6 +107,168 @@ def exchange_partials(out, imap: InterfaceMap, dist, index_tensors=None):
     return out
 
 
+class PeerExchange:
+    """Interface exchange over peer memory (NVLink / NVSwitch, CUDA IPC):
+    the compute step and the transfer in one kernel.
+
+    The surface-row kernel stores every interface row it computes straight
+    into the neighbour's receive buffer (``hhg_surface_apply_csr_push``),
+    a one-thread kernel fences and bumps the neighbour's arrival counter
+    (``hhg_p2p_signal``), and ``hhg_p2p_pull`` waits for the neighbour's
+    counter and adds the received values in rank order - the same sum as
+    :func:`exchange_partials`, so both copies of an interface row stay
+    bitwise equal.  Receive buffers are double-buffered by apply parity: a
+    rank can only push apply e+2 after it has seen the neighbour's signal
+    e+1, which the neighbour sends after finishing its pull of apply e.
+
+    Peers are connected through CUDA IPC handles exchanged with
+    ``torch.distributed`` (:meth:`connect`), or, to emulate several ranks in
+    one process on one device, directly (:meth:`connect_local`); the
+    emulation must run every rank's :meth:`start` before any :meth:`finish`
+    so no kernel ever waits on another launch of the same GPU."""
+
+    def __init__(self, op, imap: InterfaceMap):
+        import torch
+        self.torch, self.op, self.imap = torch, op, imap
+        self.rank = imap.rank
+        D = op._device()
+        rows = D["surf"].st.rows
+        pos = {int(g): r for r, g in enumerate(rows)}
+        self.nbrs = sorted(imap.neighbours)
+        slot = np.full(max(len(rows), 1), -1, dtype=np.int32)
+        base = 0
+        self.base = {}
+        for nb in self.nbrs:
+            ids = imap.neighbours[nb]
+            self.base[nb] = base
+            for m, g in enumerate(ids):
+                slot[pos[int(g)]] = base + m
+            base += len(ids)
+        dev = "cuda"
+        self.slot = torch.as_tensor(slot, device=dev)
+        self.ids = {nb: torch.as_tensor(imap.neighbours[nb], device=dev) for nb in self.nbrs}
+        self.count = {nb: len(imap.neighbours[nb]) for nb in self.nbrs}
+        # what each neighbour writes into: recv[nb] (2 parities) and its
+        # arrival counter flag[nb]; own allocations so an IPC handle maps
+        # exactly them
+        self.recv, self.flag = {}, {}
+        for nb in self.nbrs:
+            self.recv[nb] = self._alloc(16 * max(self.count[nb], 1))
+            self.flag[nb] = self._alloc(8)
+        self.err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.peer_recv, self.peer_flag = {}, {}
+        self._opened = []
+        self.epoch = 0
+
+    _owned = None
+
+    def _alloc(self, nbytes):
+        import ctypes
+        from ._lib import check, lib
+        p = ctypes.c_void_p()
+        check(lib.hhg_device_alloc(nbytes, ctypes.byref(p)), "device_alloc")
+        if self._owned is None:
+            self._owned = []
+        self._owned.append(p.value)
+        return p.value
+
+    def close(self):
+        from ._lib import lib
+        for p in self._opened:
+            lib.hhg_ipc_close_handle(p)
+        for p in self._owned or []:
+            lib.hhg_device_free(p)
+        self._opened, self._owned = [], []
+
+    # -- connection --------------------------------------------------------
+    def connect(self, dist):
+        """Exchange CUDA IPC handles of the receive buffers and counters with
+        the neighbours (all ranks call this collectively)."""
+        import ctypes
+        from ._lib import check, lib
+        mine = {}
+        for nb in self.nbrs:
+            hr, hf = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
+            check(lib.hhg_ipc_get_handle(self.recv[nb], hr), "ipc_get_handle")
+            check(lib.hhg_ipc_get_handle(self.flag[nb], hf), "ipc_get_handle")
+            mine[nb] = (hr.raw, hf.raw)
+        allh = [None] * dist.get_world_size()
+        dist.all_gather_object(allh, mine)
+        for nb in self.nbrs:
+            hr, hf = allh[nb][self.rank]                # nb's buffers that receive from me
+            pr, pf = ctypes.c_void_p(), ctypes.c_void_p()
+            check(lib.hhg_ipc_open_handle(hr, ctypes.byref(pr)), "ipc_open_handle")
+            check(lib.hhg_ipc_open_handle(hf, ctypes.byref(pf)), "ipc_open_handle")
+            self.peer_recv[nb], self.peer_flag[nb] = pr.value, pf.value
+            self._opened += [pr.value, pf.value]
+
+    def connect_local(self, peers):
+        """Single-process emulation: ``peers[nb]`` is the neighbour's
+        PeerExchange on the same device."""
+        for nb in self.nbrs:
+            other = peers[nb]
+            self.peer_recv[nb] = other.recv[self.rank]
+            self.peer_flag[nb] = other.flag[self.rank]
+
+    # -- one exchange --------------------------------------------------------
+    def _push(self):
+        par = self.epoch % 2
+        dst = [None, None]
+        for q, nb in enumerate(self.nbrs):
+            dst[q] = self.peer_recv[nb] + 8 * par * max(self.count[nb], 1)
+        split = self.base[self.nbrs[1]] if len(self.nbrs) > 1 else (1 << 62)
+        return (self.slot.data_ptr(), dst[0], dst[1], split)
+
+    def apply(self, u, out=None, volume_events=None):
+        """A u with the interface rows completed: surface rows (with the
+        pushes), the signal and the pull on a side stream while the volume
+        kernel runs (Operator.apply_device's after_surface hook)."""
+        from ._lib import check, lib
+        self.epoch += 1
+        if not self.nbrs:
+            return self.op.apply_device(u, out=out, volume_events=volume_events)
+
+        def exchange(o):
+            st = self.torch.cuda.current_stream().cuda_stream
+            for nb in self.nbrs:
+                check(lib.hhg_p2p_signal(self.peer_flag[nb], st), "p2p_signal")
+            self._pull(o, st)
+
+        return self.op.apply_device(u, out=out, push=self._push(), after_surface=exchange,
+                                    volume_events=volume_events)
+
+    def start(self, u, out=None):
+        """Apply with the interface rows pushed to the neighbours and signal
+        them; returns the output (interface rows still one-sided)."""
+        from ._lib import check, lib
+        self.epoch += 1
+        out = self.op.apply_device(u, out=out, push=self._push() if self.nbrs else None)
+        st = self.torch.cuda.current_stream().cuda_stream
+        for nb in self.nbrs:
+            check(lib.hhg_p2p_signal(self.peer_flag[nb], st), "p2p_signal")
+        return out
+
+    def finish(self, out):
+        """Wait for the neighbours' values of this apply and complete the
+        interface rows in rank order."""
+        self._pull(out, self.torch.cuda.current_stream().cuda_stream)
+        return out
+
+    def _pull(self, out, st):
+        from ._lib import check, lib
+        par = self.epoch % 2
+        for nb in self.nbrs:
+            check(lib.hhg_p2p_pull(out.data_ptr(), self.ids[nb].data_ptr(), self.count[nb],
+                                   self.recv[nb] + 8 * par * max(self.count[nb], 1),
+                                   self.flag[nb], self.epoch, int(nb < self.rank),
+                                   self.err.data_ptr(), st), "p2p_pull")
+
+    def check(self):
+        """Raise if a pull timed out (call after synchronising)."""
+        if int(self.err.item()):
+            raise RuntimeError("peer exchange: neighbour values did not arrive")
+
+
 class ShardedOperator:
     """One rank's share of a partitioned operator: the local slab operator
     plus the interface exchange.
@@ -118,11 +280,17 @@ class ShardedOperator:
     first and the exchange runs on a side stream while the volume kernel
     computes the (communication-free) volume rows."""
 
-    def __init__(self, op, imap: InterfaceMap, dist, dirichlet_mask):
+    def __init__(self, op, imap: InterfaceMap, dist, dirichlet_mask, transport="nccl"):
         import torch
         self.op, self.imap, self.dist = op, imap, dist
         self.torch = torch
         self._idx, self._masks = {}, {}
+        if transport not in ("nccl", "p2p"):
+            raise ValueError("transport must be 'nccl' or 'p2p'")
+        self.peer = None
+        if transport == "p2p":
+            self.peer = PeerExchange(op, imap)
+            self.peer.connect(dist)
         self._dirichlet = np.asarray(dirichlet_mask, dtype=bool)
         self._owned = imap.owned_mask(len(self._dirichlet)) & ~self._dirichlet
 
@@ -143,6 +311,8 @@ class ShardedOperator:
     def apply(self, u):
         """A u with the interface rows completed (identity Dirichlet rows)."""
         torch = self.torch
+        if u.is_cuda and self.peer is not None:
+            return self.peer.apply(u)
         if u.is_cuda and hasattr(self.op, "apply_device"):
             idx = self._index(u.device)
             # runs on the operator's side stream right after the surface
