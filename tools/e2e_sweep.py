@@ -1,3 +1,6 @@
+"""Host-buffer apply (Operator.apply on a pinned CPU tensor, the e2e leg of
+bench.py) for several element-group counts of the H2D / kernel / D2H
+pipeline on the config-5 workload."""
 import sys, time, statistics
 sys.path.insert(0, ".")
 import numpy as np, torch

@@ -1,3 +1,5 @@
+"""Build the data-movement-only volume kernel (HHG_VOL_EXPT=1) and run it
+on the config-5 workload, for an ncu capture of the staging path alone."""
 import ctypes, subprocess, sys
 from pathlib import Path
 import numpy as np, torch

@@ -1,3 +1,5 @@
+"""Summarise an ncu report: headline metrics and the SASS instruction mix
+with stall shares.  Usage: python tools/ncu_summary.py report.ncu-rep"""
 import csv, collections, subprocess, sys
 rep = sys.argv[1]
 raw = subprocess.run(["ncu","-i",rep,"--page","raw","--csv"],capture_output=True,text=True).stdout

@@ -1,3 +1,4 @@
+"""Time the nodal-integration volume kernel on a small workload."""
 import sys, time
 from pathlib import Path
 import numpy as np, torch
