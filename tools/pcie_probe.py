@@ -39,3 +39,25 @@ def both():
 
 t = timeit(both)
 print(f"H2D+D2H     {2 * gb / t:6.1f} GB/s total  {t * 1e3:6.1f} ms (2 x {gb:.2f} GB)")
+
+
+# several concurrent D2H / H2D copies (separate copy engines?)
+for ns in (2, 4):
+    streams = [torch.cuda.Stream() for _ in range(ns)]
+    chunk = n // ns
+
+    def multi_d2h():
+        for i, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                h_out[i * chunk:(i + 1) * chunk].copy_(d_out[i * chunk:(i + 1) * chunk],
+                                                       non_blocking=True)
+
+    def multi_h2d():
+        for i, st in enumerate(streams):
+            with torch.cuda.stream(st):
+                d_in[i * chunk:(i + 1) * chunk].copy_(h_in[i * chunk:(i + 1) * chunk],
+                                                      non_blocking=True)
+    t = timeit(multi_d2h)
+    print(f"D2H {ns} streams {gb / t:6.1f} GB/s  {t * 1e3:6.1f} ms")
+    t = timeit(multi_h2d)
+    print(f"H2D {ns} streams {gb / t:6.1f} GB/s  {t * 1e3:6.1f} ms")
