@@ -60,7 +60,7 @@ __device__ __forceinline__ double *gs_addr(const GSDesc &D, int t, int i, int j,
 
 // block size: the nodal row's 55-slot buffer needs > 64 registers
 template <int VAR, bool COOP>
-constexpr int gs_volume_threads() { return (VAR == 0 ? 512 : 256) / (COOP ? 2 : 1); }
+constexpr int gs_volume_threads() { return COOP ? 128 : 256; }
 
 // One macro element per CTA group: D.cpt co-resident CTAs share an
 // element (blockIdx.x = t * cpt + c) and split every hyperplane's points;
@@ -93,58 +93,88 @@ gs_volume_kernel(GSDesc D) {
   const double *kt = D.kc + (long long)t * D.L;
   const int stride = cpt * blockDim.x;
   const int first = part * blockDim.x + threadIdx.x;
-  for (int h = hmin; h <= hmax; ++h) {
-    const int ha = D.hp_ptr[h - hmin], hb = D.hp_ptr[h - hmin + 1];
-    for (int e = ha + first; e < hb; e += stride) {
-      const int code = __ldg(D.hp_code + e);
-      const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
-      // 32-bit plane constants of planes k-1, k, k+1 (as the surface rows)
-      const IncPlanes P = inc_planes(n, k);
-      double *ut = D.lattice ? D.u + (long long)t * D.L : D.u + D.vol_start[t];
-      const double *gt = D.ghost + (long long)t * D.S;
-      double *up;
+  double *ut = D.lattice ? D.u + (long long)t * D.L : D.u + D.vol_start[t];
+  const double *gt = D.ghost + (long long)t * D.S;
+  const double *ft = D.lattice ? D.f + (long long)t * D.nvol : D.f + D.vol_start[t];
+
+  // static part of a point (code, k at the point and its neighbours, f):
+  // for the thread's first point of the next hyperplane it is loaded
+  // before the barrier, so only the neighbour values remain behind it
+  struct Static {
+    int code;
+    double k0, fv;
+    double kq[14];
+  };
+  auto load_static = [&](int e, Static &S) {
+    S.code = __ldg(D.hp_code + e);
+    const int i = S.code & 1023, j = (S.code >> 10) & 1023, k = (S.code >> 20) & 1023;
+    const IncPlanes P = inc_planes(n, k);
+    S.k0 = __ldg(kt + inc_koff(P, 1, i, j));
+#pragma unroll
+    for (int d = 0; d < 14; ++d)
+      S.kq[d] = __ldg(kt + inc_koff(P, c_dirs_h(d, 2) + 1, i + c_dirs_h(d, 0),
+                                    j + c_dirs_h(d, 1)));
+    S.fv = __ldg(ft + lbase32(n - 4, k - 1, j - 1) + i - 1);
+  };
+  auto update = [&](const Static &S) {
+    const int i = S.code & 1023, j = (S.code >> 10) & 1023, k = (S.code >> 20) & 1023;
+    const IncPlanes P = inc_planes(n, k);
+    double *up;
+    if (D.lattice) {
+      up = ut + inc_koff(P, 1, i, j);
+    } else {
+      int off;
+      inc_voff(P, 1, n, i, j, k, off);              // interior point
+      up = ut + off;
+    }
+    double2 q[14];
+#pragma unroll
+    for (int d = 0; d < 14; ++d) {
+      const int dk = c_dirs_h(d, 2);
+      const int qi = i + c_dirs_h(d, 0), qj = j + c_dirs_h(d, 1), qk = k + dk;
       if (D.lattice) {
-        up = ut + inc_koff(P, 1, i, j);
+        const int ko = inc_koff(P, dk + 1, qi, qj);
+        q[d].x = COOP ? __ldcg(ut + ko) : ut[ko];
       } else {
         int off;
-        inc_voff(P, 1, n, i, j, k, off);              // interior point
-        up = ut + off;
+        const bool in = inc_voff(P, dk + 1, n, qi, qj, qk, off);
+        q[d].x = in ? (COOP ? __ldcg(ut + off) : ut[off]) : __ldg(gt + off);
       }
-      const double k0 = __ldg(kt + inc_koff(P, 1, i, j));
-      double2 q[14];
+      q[d].y = S.kq[d];
+    }
+    double acc = 0.0, diag = 0.0;
+    if (VAR == 0) {
 #pragma unroll
       for (int d = 0; d < 14; ++d) {
-        const int dk = c_dirs_h(d, 2);
-        const int qi = i + c_dirs_h(d, 0), qj = j + c_dirs_h(d, 1), qk = k + dk;
-        const int ko = inc_koff(P, dk + 1, qi, qj);
-        if (D.lattice) {
-          q[d].x = COOP ? __ldcg(ut + ko) : ut[ko];
-        } else {
-          int off;
-          const bool in = inc_voff(P, dk + 1, n, qi, qj, qk, off);
-          q[d].x = in ? (COOP ? __ldcg(ut + off) : ut[off]) : __ldg(gt + off);
-        }
-        q[d].y = __ldg(kt + ko);
+        const double sd = dmul(dadd(S.k0, q[d].y), coef[d]);
+        acc = dadd(acc, dmul(sd, q[d].x));
+        diag = dsub(diag, sd);
       }
-      double acc = 0.0, diag = 0.0;
-      if (VAR == 0) {
-#pragma unroll
-        for (int d = 0; d < 14; ++d) {
-          const double sd = dmul(dadd(k0, q[d].y), coef[d]);
-          acc = dadd(acc, dmul(sd, q[d].x));
-          diag = dsub(diag, sd);
-        }
-      } else {
-        double b[55];
-        nodal_buffer(k0, q, b);
-        nodal_gs_terms<0>(acc, diag, q, b, sfac);
-      }
-      if (diag == 0.0) atomicOr(&g_status, 1);
-      const long long c = lbase32(n - 4, k - 1, j - 1) + i - 1;
-      const double fv = D.lattice ? D.f[(long long)t * D.nvol + c]
-                                  : D.f[D.vol_start[t] + c];
-      const double old = COOP ? __ldcg(up) : *up;
-      *up = dadd(dmul(dsub(1.0, omega), old), ddiv(dmul(omega, dsub(fv, acc)), diag));
+    } else {
+      double b[55];
+      nodal_buffer(S.k0, q, b);
+      nodal_gs_terms<0>(acc, diag, q, b, sfac);
+    }
+    if (diag == 0.0) atomicOr(&g_status, 1);
+    const double old = COOP ? __ldcg(up) : *up;
+    *up = dadd(dmul(dsub(1.0, omega), old), ddiv(dmul(omega, dsub(S.fv, acc)), diag));
+  };
+
+  Static pre;
+  bool have = hmin <= hmax && D.hp_ptr[0] + first < D.hp_ptr[1];
+  if (have) load_static(D.hp_ptr[0] + first, pre);
+  for (int h = hmin; h <= hmax; ++h) {
+    const int ha = D.hp_ptr[h - hmin], hb = D.hp_ptr[h - hmin + 1];
+    if (have) update(pre);
+    for (int e = ha + first + stride; e < hb; e += stride) {
+      Static S;
+      load_static(e, S);
+      update(S);
+    }
+    if (h < hmax) {
+      const int na = D.hp_ptr[h + 1 - hmin], nb = D.hp_ptr[h + 2 - hmin];
+      have = na + first < nb;
+      if (have) load_static(na + first, pre);
     }
     if constexpr (COOP) cooperative_groups::this_grid().sync();
     else __syncthreads();
