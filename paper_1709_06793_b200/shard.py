@@ -132,17 +132,18 @@ class PeerExchange:
         self.torch, self.op, self.imap = torch, op, imap
         self.rank = imap.rank
         D = op._device()
-        rows = D["surf"].st.rows
-        pos = {int(g): r for r, g in enumerate(rows)}
+        rows = np.asarray(D["surf"].st.rows)          # ascending global ids
         self.nbrs = sorted(imap.neighbours)
         slot = np.full(max(len(rows), 1), -1, dtype=np.int32)
         base = 0
         self.base = {}
         for nb in self.nbrs:
-            ids = imap.neighbours[nb]
+            ids = np.asarray(imap.neighbours[nb])
+            r = np.searchsorted(rows, ids)
+            if len(ids) and (r.max() >= len(rows) or np.any(rows[r] != ids)):
+                raise ValueError("interface node is not a free surface row")
             self.base[nb] = base
-            for m, g in enumerate(ids):
-                slot[pos[int(g)]] = base + m
+            slot[r] = base + np.arange(len(ids), dtype=np.int32)
             base += len(ids)
         dev = "cuda"
         self.slot = torch.as_tensor(slot, device=dev)
