@@ -177,3 +177,13 @@ def test_two_rank_cg_matches_single_domain():
         assert np.abs(xr - ustar[gids]).max() <= 1e-7     # solves A x = A u*
         assert true_res <= 1e-9 * b0
     assert res[0][3] == res[1][3]                         # ranks agree on the count
+
+
+def test_sharded_operator_rejects_unknown_transport():
+    from paper_1709_06793_b200.mesh import RefinedGrid
+    from paper_1709_06793_b200.shard import InterfaceMap, ShardedOperator, slab_mesh
+    grid = RefinedGrid(slab_mesh(0, 1, nx=2, ny=2), 2)
+    imap = InterfaceMap(grid, 0, 1, 0.5)
+    assert imap.neighbours == {}
+    with pytest.raises(ValueError, match="transport"):
+        ShardedOperator(object(), imap, None, grid.dirichlet_mask, transport="mpi")
