@@ -218,13 +218,6 @@ class SurfaceTables:
         return np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
 
 
-def partial_tables(op_tables):
-    """Stack per-element partial stencils (psh, pfac)."""
-    psh = np.ascontiguousarray(np.stack([p for p, _ in op_tables]))
-    pfac = np.ascontiguousarray(np.stack([f for _, f in op_tables]))
-    return psh, pfac
-
-
 class DeviceGrid:
     """Torch buffers + the hhg_grid descriptor of one level."""
 
