@@ -13,6 +13,12 @@ rows, and (N > 1) the interface exchange.  `value` counts volume unknowns
 ranks; `e2e` times the public call with host numpy buffers.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+With --gpus N > 1 and no torchrun environment the script re-launches itself
+under `torch.distributed.run` with N local ranks (127.0.0.1 rendezvous) and
+exits with its status; under torchrun it checks WORLD_SIZE == N.
+`--dry-run` runs the same multi-rank plumbing on CPU (gloo, no kernels): the
+interface partial-sum exchange of every rank's slab at a tiny level.
 """
 from __future__ import annotations
 
@@ -49,13 +55,38 @@ def parse():
                          "surface-row kernel (CUDA IPC over NVLink) or NCCL send/recv")
     ap.add_argument("--cpu-tets", type=int, default=16,
                     help="macro elements per CPU-baseline step (bounded sample)")
-    return ap.parse_args()
+    ap.add_argument("--bitwise", action="store_true",
+                    help="reference-order arithmetic (bitwise the CPU kernel); default "
+                         "is the FMA edge-flux form, within 1e-12 of it")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU/gloo multi-rank plumbing check (no GPU work)")
+    a = ap.parse_args()
+    if a.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    a.fast = not a.bitwise          # --fast kept for compatibility (it is the default)
+    return a
 
 
-def dist_env():
+def relaunch(args):
+    """--gpus N > 1 outside torchrun: run N local ranks under
+    torch.distributed.run (one process per GPU) and return its status."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def dist_env(args=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args is not None and "WORLD_SIZE" in os.environ and world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        sys.exit(2)
     return world, rank, local
 
 
@@ -129,16 +160,19 @@ def build_workload(rank, world, level, nx, variant, fast):
 
 def run_own(args):
     import torch
-    world, rank, local = dist_env()
+    world, rank, local = dist_env(args)
     dist = None
     if world > 1:
         import torch.distributed as dist
+        if torch.cuda.device_count() < world:
+            sys.stderr.write(f"bench.py: {world} ranks but {torch.cuda.device_count()} GPUs\n")
+            sys.exit(2)
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     from paper_1709_06793_b200._lib import lib
-    from paper_1709_06793_b200.costmodel import volume_apply_bytes
+    from paper_1709_06793_b200.costmodel import volume_apply_bytes, apply_step_bytes
     from paper_1709_06793_b200.shard import exchange_partials
 
     t_setup = time.time()
@@ -177,23 +211,36 @@ def run_own(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    if sop is not None:
+        sop.check()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.hhg_launch_count()
     with ClockSampler(local) as clk:
         ev0.record()
         for _ in range(args.steps):
             step(record=True)
         ev1.record()
         torch.cuda.synchronize()
+    launches = lib.hhg_launch_count() - launches0
+    if sop is not None:
+        sop.check()                       # a lost peer signal invalidates the run
     ms = ev0.elapsed_time(ev1) / args.steps
     vol_ms = sum(a.elapsed_time(b) for a, b in vol_ev) / len(vol_ev)
+    per_rank = [{"rank": rank, "step_ms": round(ms, 4), "volume_kernel_ms": round(vol_ms, 4),
+                 "other_ms": round(ms - vol_ms, 4)}]
     if dist:
         dist.barrier()
         t = torch.tensor([ms, vol_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, vol_ms = t.tolist()
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank = [{"rank": r, "step_ms": round(float(x[0]), 4),
+                     "volume_kernel_ms": round(float(x[1]), 4),
+                     "other_ms": round(float(x[0] - x[1]), 4)} for r, x in enumerate(allt)]
+        ms = max(float(x[0]) for x in allt)         # max over ranks
+        vol_ms = max(float(x[1]) for x in allt)
 
     ntets = grid.macro.n_elements
     nvol_rank = grid.nodes_per_volume * ntets
@@ -202,6 +249,7 @@ def run_own(args):
     hbm, hbm_kind = peaks()
     bytes_launch = volume_apply_bytes(args.level, ntets)
     achieved = bytes_launch / (vol_ms * 1e-3) / 1e9
+    step_bytes = apply_step_bytes(grid, op)
 
     # end to end through the public API with HOST buffers: pinned CPU tensor
     # in, Operator.apply (H2D, kernels, D2H into pinned memory) out
@@ -222,25 +270,29 @@ def run_own(args):
         torch.cuda.synchronize()
         if i:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        del res
     e2e = statistics.median(e2e_ms)
     if dist:
         t = torch.tensor([e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = t.item()
-    assert tuple(res.shape) == (grid.n_nodes,)
 
     traffic = None
     tp = ROOT / "profiles" / "volume_traffic.json"
     if tp.exists():
         tj = json.loads(tp.read_text())
-        if tj.get("level") == args.level and tj.get("ntets") == ntets:
+        if tj.get("level") == args.level and tj.get("ntets") == ntets and \
+                tj.get("arithmetic") == ("fma" if args.fast else "bitwise"):
             traffic = tj.get("dram_bytes_per_launch")
 
     cpu = None
     if rank == 0 and world == 1:
-        cpu = cpu_baseline(grid, kf, op, u, args.cpu_tets, reps=2)
+        cpu = cpu_baseline(grid, kf, op, u, args.cpu_tets, reps=3)
 
     if rank == 0:
+        flags = op._vol_flags()
+        arith = ("fma edge-flux, mirror edge reuse (<= 1e-12 of the reference order)"
+                 if flags & 2 else "bitwise-reference-order, mirror edge reuse")
         line = {
             "metric": "GDoF/s of scaled-stencil apply (fp64)",
             "value": round(value, 3), "unit": "GDoF/s", "n_gpus": world,
@@ -251,20 +303,24 @@ def run_own(args):
                                    f"level {args.level}", "level": args.level,
                        "macro_tets_per_gpu": ntets, "dofs_per_gpu": int(grid.n_nodes),
                        "volume_dofs_per_gpu": int(nvol_rank), "variant": args.variant,
-                       "arithmetic": "fast-fma" if args.fast else
-                       ("bitwise-reference-order, mirror edge reuse"
-                        if op._vol_flags() & 4 else "bitwise-reference-order"),
-                       "parallelism": f"macro-tet slabs x{world}",
+                       "arithmetic": arith,
+                       "parallelism": f"macro-tet slabs x{world}"
+                                      + (f", {args.exchange} interface exchange" if world > 1
+                                         else ""),
                        "l2": "inputs larger than L2 (2.2 GB per vector)"},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                          "unit": "GB/s", "frac": round(achieved / hbm, 4),
                          "traffic": traffic, "peak_kind": hbm_kind,
-                         "kernel": "volume_kernel", "kernel_ms": round(vol_ms, 4),
-                         "algorithmic_bytes_per_launch": bytes_launch},
+                         "kernel": "volume_kernel_mirror", "kernel_ms": round(vol_ms, 4),
+                         "algorithmic_bytes_per_launch": bytes_launch,
+                         "step": {"algorithmic_bytes": step_bytes,
+                                  "achieved": round(step_bytes / (ms * 1e-3) / 1e9, 1),
+                                  "frac": round(step_bytes / (ms * 1e-3) / 1e9 / hbm, 4)}},
             "e2e": {"value": round(total_dofs / (e2e * 1e-3) / 1e9, 4), "unit": "GDoF/s",
                     "ms_per_step": round(e2e, 2), "h2d_bytes_per_step": 8 * grid.n_nodes,
                     "d2h_bytes_per_step": 8 * grid.n_nodes},
-            "gpu_launches": args.steps * 4,   # ghost, volume, surface rows, Dirichlet rows
+            "gpu_launches": int(launches),
+            "per_rank": per_rank,
             "all_rows_gdofs": round(grid.n_nodes * world / (ms * 1e-3) / 1e9, 3),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
@@ -273,6 +329,52 @@ def run_own(args):
         }
         print(json.dumps(line), flush=True)
     if dist:
+        dist.destroy_process_group()
+
+
+def run_dry(args):
+    """--dry-run: the multi-rank plumbing of the bench on CPU (gloo): every
+    rank builds its slab at --level, exchanges and completes its interface
+    partial sums with the neighbours, times the steps on the host and takes
+    the max over ranks; no GPU work, no measured value."""
+    import torch
+    import torch.distributed as dist
+    from paper_1709_06793_b200 import RefinedGrid
+    from paper_1709_06793_b200.shard import InterfaceMap, exchange_partials, slab_mesh
+    world, rank, _ = dist_env(args)
+    if world > 1:
+        dist.init_process_group("gloo")
+    grid = RefinedGrid(slab_mesh(rank, world, args.nx, args.nx), args.level)
+    imap = InterfaceMap(grid, rank, world, 1.0 / args.nx) if world > 1 else None
+    vec = torch.as_tensor(np.random.default_rng(rank).uniform(-1, 1, grid.n_nodes))
+    idx = {k: torch.as_tensor(v) for k, v in imap.neighbours.items()} if imap else None
+    for _ in range(args.warmup):
+        if imap:
+            exchange_partials(vec.clone(), imap, dist, idx)
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        if imap:
+            exchange_partials(vec.clone(), imap, dist, idx)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    ranks = [rank]
+    if world > 1:
+        t = torch.tensor([ms])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+        allr = [None] * world
+        dist.all_gather_object(allr, rank)
+        ranks = allr
+    if rank == 0:
+        print(json.dumps({"metric": "GDoF/s of scaled-stencil apply (fp64)", "dry_run": True,
+                          "value": None, "unit": "GDoF/s", "n_gpus": world,
+                          "ranks_seen": ranks, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": round(ms, 4), "scaling": "weak",
+                          "config": {"workload": f"dry run: slab of {grid.macro.n_elements} "
+                                                 f"macro tets per rank, level {args.level}",
+                                     "parallelism": f"macro-tet slabs x{world}"}}), flush=True)
+    if world > 1:
         dist.destroy_process_group()
 
 
@@ -305,6 +407,7 @@ def run_reference(args):
     and is not importable on the GPU box) on all host cores, same config,
     metric and units; rank 0 only."""
     world, rank, _ = dist_env()
+    world = max(world, args.gpus)
     if rank != 0:
         return
     from oracle import kernels as ok
@@ -347,6 +450,10 @@ def run_reference(args):
 if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
-        run_reference(a)
+        run_reference(a)          # rank 0 of N (or a plain process): host cores only
+    elif a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(a))
+    elif a.dry_run:
+        run_dry(a)
     else:
         run_own(a)

@@ -78,7 +78,7 @@ int hhg_apply_nodal_3d(int64_t n, const int64_t *base, const double *v,
                        void *stream);
 
 /* replaces kernels.apply_const_3d(n, base, v, s, c0, out), kernels.py:22-53;
- * s is a device pointer to 14 doubles */
+ * s is a device pointer to the 14 neighbour weights, c0 the diagonal weight */
 int hhg_apply_const_3d(int64_t n, const int64_t *base, const double *v,
                        const double *s, double c0, double *out, void *stream);
 
@@ -86,6 +86,15 @@ int hhg_apply_const_3d(int64_t n, const int64_t *base, const double *v,
  * w is float64[nvol][15] */
 int hhg_apply_stored_3d(int64_t n, const int64_t *base, const double *v,
                         const double *w, double *out, void *stream);
+
+/* replaces kernels.csr_gs(rows, indptr, indices, data, diag, u, f, omega),
+ * kernels.py:979-992: forward Gauss-Seidel over rows[0..nrows_list) of a
+ * CSR matrix (int64 indptr / indices, float64 data; diag indexed by row id)
+ * in list order, bitwise the sequential loop; a zero diagonal stops the
+ * sweep at that row and is reported by hhg_status (HHG_ERR_ZERO_DIAG). */
+int hhg_csr_gs(int64_t nrows_list, const int64_t *rows, const int64_t *indptr,
+               const int64_t *indices, const double *data, const double *diag,
+               double *u, const double *f, double omega, void *stream);
 
 /* replaces kernels.gs_scaling_3d(n, base, u, fv, kc, sh, omega),
  * kernels.py:510-550: forward lexicographic Gauss-Seidel in place on the
@@ -329,6 +338,10 @@ int hhg_volume_tile_cols_mirror(void);
  * after synchronising the stream */
 int hhg_status(void);
 int hhg_status_reset(void);
+
+/* number of kernel launches this library has issued in the process
+ * (host-side counter; every launch site counts one) */
+long long hhg_launch_count(void);
 
 /* compile-time kernel configuration, for reports */
 const char *hhg_build_info(void);

@@ -59,6 +59,8 @@ EXPORTS = {
     "hhg_apply_const_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp,
                                           ctypes.c_double, vp, vp]),
     "hhg_apply_stored_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),
+    "hhg_csr_gs": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp,
+                                  ctypes.c_double, vp]),
     "hhg_gs_scaling_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp,
                                          ctypes.c_double, vp]),
     "hhg_gs_nodal_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, c_i64p,
@@ -116,6 +118,7 @@ EXPORTS = {
                                     ctypes.c_int, vp, vp]),
     "hhg_device_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
     "hhg_device_free": (ctypes.c_int, [vp]),
+    "hhg_launch_count": (ctypes.c_longlong, []),
     "hhg_ipc_get_handle": (ctypes.c_int, [vp, vp]),
     "hhg_ipc_open_handle": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_void_p)]),
     "hhg_ipc_close_handle": (ctypes.c_int, [vp]),

@@ -75,3 +75,23 @@ def volume_apply_bytes(level: int, n_tets: int, residual: bool = False) -> int:
 def operations_table():
     return [{"dim": d, "variant": v, "adds": a, "mults": m, "total": a + m}
             for (v, d), (a, m) in sorted(_ANALYTIC.items(), key=lambda kv: (-kv[0][1], kv[0][0]))]
+
+
+def apply_step_bytes(grid, op) -> int:
+    """Bytes one full device-resident Operator.apply moves with this
+    implementation's data structures (bench.py's step-level roofline): the
+    volume kernel (volume_apply_bytes), the ghost-layer update (gather list
+    8 B + u 8 B + ghost write 8 B per shell point), the precomputed surface
+    rows (per entry a 4-B column, an 8-B weight and the 8-B neighbour value;
+    per row its 8-B offset, 8-B id, centre value and result) and the
+    Dirichlet identity rows (8-B id, read, write)."""
+    D = op._device()
+    gt = D["grid"].gt
+    st = D["surf"].st
+    nent = int(st.entry_ptr()[-1])
+    nrows = len(st.rows)
+    vol = volume_apply_bytes(grid.level, gt.ntets)
+    ghost = 24 * gt.ntets * gt.S
+    surf = 20 * nent + 32 * nrows
+    dirich = 24 * len(st.dir_ids)
+    return int(vol + ghost + surf + dirich)

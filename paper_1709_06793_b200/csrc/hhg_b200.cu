@@ -6,7 +6,10 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <map>
+#include <mutex>
+#include <set>
 #include <tuple>
 #include <vector>
 
@@ -16,6 +19,12 @@
 #include "hhg_surface.cuh"
 #include "hhg_tensor.cuh"
 #include "hhg_volume.cuh"
+#ifndef HHG_VOLUME_TMA
+#define HHG_VOLUME_TMA 0   // experimental TMA-staged kernel (profiles/README.md, round 2)
+#endif
+#if HHG_VOLUME_TMA
+#include "hhg_volume_tma.cuh"
+#endif
 
 using namespace hhg;
 
@@ -36,7 +45,26 @@ using namespace hhg;
 static constexpr int kB = HHG_VOL_B, kW = HHG_VOL_W, kNS = HHG_VOL_NS;
 
 static inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+// dynamic shared-memory opt-in of a kernel, once per (device, kernel)
+static std::mutex g_attr_mu;
+static int smem_optin(const void *kern, int bytes) {
+  static std::set<std::pair<int, const void *>> done;
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (done.count({dev, kern})) return HHG_OK;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) !=
+      cudaSuccess)
+    return HHG_ERR_CUDA;
+  done.insert({dev, kern});
+  return HHG_OK;
+}
+
+// every kernel launch of the library goes through check(): it also counts
+// them (hhg_launch_count, bench.py's gpu_launches)
+static std::atomic<long long> g_launches{0};
 static inline int check(const char *what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     fprintf(stderr, "hhg_b200: %s: %s\n", what, cudaGetErrorString(e));
@@ -68,11 +96,7 @@ static int launch_volume(const VolDesc &D, cudaStream_t st) {
   const size_t smem = sizeof(double2) * kNS * ROWS * VOL_COLS + 72 * sizeof(double);
   constexpr int MINB = (VAR == 1) ? 1 : HHG_VOL_MINB;
   auto kern = volume_kernel<VAR, SRC, RES, FAST, B, W, kNS, MINB, MIRROR>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  if (smem_optin((const void *)kern, (int)smem)) return HHG_ERR_CUDA;
   kern<<<D.ntiles, 32 * W, smem, st>>>(D);
   return check("volume_kernel");
 }
@@ -83,8 +107,11 @@ static int launch_volume(const VolDesc &D, cudaStream_t st) {
 #ifndef HHG_MIRROR_MINB
 #define HHG_MIRROR_MINB (8 / HHG_MIRROR_NW)
 #endif
+#ifndef HHG_MIRROR_FMA_MINB
+#define HHG_MIRROR_FMA_MINB HHG_MIRROR_MINB
+#endif
 
-template <int SRC, bool RES>
+template <int SRC, bool RES, int MODE = 0>
 static int launch_mirror(const VolDesc &D, cudaStream_t st) {
   if (D.nmtiles <= 0) return D.ntiles > 0 ? HHG_ERR_ARG : HHG_OK;
   static_assert(kW == 4, "the mirror kernel uses 8x4-lane warps of 4B rows");
@@ -94,25 +121,87 @@ static int launch_mirror(const VolDesc &D, cudaStream_t st) {
 #ifndef HHG_VOLUME_WS
 #define HHG_VOLUME_WS 0          // warp-specialised producer / consumer form
 #endif
-  if (HHG_VOLUME_WS && NW == 4) {
+  if (HHG_VOLUME_WS && NW == 4 && MODE == 0) {
     auto kern = volume_kernel_ws<SRC, RES, kB, kNS>;
-    static bool configured_ws = false;
-    if (!configured_ws) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      configured_ws = true;
-    }
+    if (smem_optin((const void *)kern, (int)smem)) return HHG_ERR_CUDA;
     kern<<<D.nmtiles, 256, smem, st>>>(D);
     return check("volume_kernel_ws");
   }
-  auto kern = volume_kernel_mirror<SRC, RES, kB, kNS, HHG_MIRROR_MINB, NW>;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    configured = true;
-  }
+  constexpr int MB = MODE == 1 ? HHG_MIRROR_FMA_MINB : HHG_MIRROR_MINB;
+  auto kern = volume_kernel_mirror<SRC, RES, kB, kNS, MB, NW, MODE>;
+  if (smem_optin((const void *)kern, (int)smem)) return HHG_ERR_CUDA;
   kern<<<D.nmtiles, 32 * NW, smem, st>>>(D);
   return check("volume_kernel_mirror");
 }
+
+#if HHG_VOLUME_TMA
+// ---------------------------------------------------------------------------
+// TMA-staged scaling kernel (hhg_volume_tma.cuh): 1-D tensor maps over the
+// global vector, the ghost shells and the coefficient lattices, encoded per
+// call (host-side, ~1 us each; the u pointer changes between calls)
+// ---------------------------------------------------------------------------
+#ifndef HHG_TMA_NS
+#define HHG_TMA_NS 6
+#endif
+#ifndef HHG_TMA_MINB
+#define HHG_TMA_MINB 2
+#endif
+#ifndef HHG_TMA_L2PROMO
+#define HHG_TMA_L2PROMO 2        // CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+#endif
+
+static PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+static bool tma_map_1d(CUtensorMap *m, const void *base, long long len) {
+  auto enc = tma_encoder();
+  if (!enc || len <= 0) return false;
+  cuuint64_t dim[1] = {(cuuint64_t)len};
+  cuuint64_t stride[1] = {(cuuint64_t)len * 8};   // unused for rank 1
+  cuuint32_t box[1] = {(cuuint32_t)TMA_BOX}, es[1] = {1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 1, const_cast<void *>(base), dim, stride, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             (CUtensorMapL2promotion)HHG_TMA_L2PROMO,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// TMA coordinates are 32-bit element indices
+static bool tma_fits(const VolDesc &D) {
+  const long long lim = (1LL << 31) - 64;
+  return D.n_nodes > 0 && D.n_nodes < lim && (long long)D.ntets * D.L < lim &&
+         (long long)D.ntets * D.S < lim && D.n >= 8 && D.nmtiles > 0;
+}
+
+template <bool RES, int MODE>
+static int launch_tma(const VolDesc &D, cudaStream_t st) {
+  static_assert(HHG_MIRROR_NW == 4, "the TMA kernel uses the 32-column mirror tiles");
+  TmaMaps M;
+  if (!tma_map_1d(&M.u, D.u, D.n_nodes) || !tma_map_1d(&M.g, D.ghost, (long long)D.ntets * D.S) ||
+      !tma_map_1d(&M.k, D.kc, (long long)D.ntets * D.L))
+    return HHG_ERR_CUDA;
+  constexpr unsigned smem = TmaGeom<kB>::smem_bytes<HHG_TMA_NS>();
+  auto kern = volume_kernel_tma<RES, MODE, kB, HHG_TMA_NS, HHG_TMA_MINB>;
+  if (smem_optin((const void *)kern, (int)smem)) return HHG_ERR_CUDA;
+  kern<<<D.nmtiles, 256, smem, st>>>(M, D);
+  return check("volume_kernel_tma");
+}
+#else
+static bool tma_fits(const VolDesc &) { return false; }
+template <bool RES, int MODE>
+static int launch_tma(const VolDesc &, cudaStream_t) { return HHG_ERR_ARG; }
+#endif
 
 template <int SRC>
 static int dispatch_volume(const VolDesc &D, int variant, int flags, cudaStream_t st) {
@@ -121,12 +210,21 @@ static int dispatch_volume(const VolDesc &D, int variant, int flags, cudaStream_
   const bool mirror = flags & HHG_FLAG_MIRROR;
 #ifdef HHG_SCALING_ONLY  // tuning builds (tools/tune_volume.py)
   if (variant != HHG_VAR_SCALING || res || SRC != SRC_SPLIT) return HHG_ERR_ARG;
+  if (mirror && HHG_VOLUME_TMA && tma_fits(D))
+    return fast ? launch_tma<false, 1>(D, st) : launch_tma<false, 0>(D, st);
+  if (mirror && fast) return launch_mirror<SRC, false, 1>(D, st);
   if (fast) return launch_volume<0, SRC, false, true>(D, st);
   return mirror ? launch_mirror<SRC, false>(D, st)
                 : launch_volume<0, SRC, false, false>(D, st);
 #endif
   switch (variant) {
     case HHG_VAR_SCALING:
+      if (SRC == SRC_SPLIT && mirror && HHG_VOLUME_TMA && tma_fits(D)) {
+        if (fast) return res ? launch_tma<true, 1>(D, st) : launch_tma<false, 1>(D, st);
+        return res ? launch_tma<true, 0>(D, st) : launch_tma<false, 0>(D, st);
+      }
+      if (mirror && fast) return res ? launch_mirror<SRC, true, 1>(D, st)
+                                     : launch_mirror<SRC, false, 1>(D, st);
       if (fast) return res ? launch_volume<0, SRC, true, true>(D, st)
                            : launch_volume<0, SRC, false, true>(D, st);
       if (mirror) return res ? launch_mirror<SRC, true>(D, st)
@@ -179,16 +277,28 @@ struct ElemTiles {
   int count = 0;
 };
 
+// process-lifetime caches are keyed by the current device as well (device
+// pointers of one GPU are not valid on another) and guarded by one mutex
+// (ctypes releases the GIL around these calls)
+static std::mutex g_cache_mu;
+static int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
 static int elem_tiles(int n, const int4 **tiles, int *count) {
-  static std::map<int, ElemTiles> cache;
-  auto it = cache.find(n);
+  static std::map<std::pair<int, int>, ElemTiles> cache;
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  const auto key = std::make_pair(current_device(), n);
+  auto it = cache.find(key);
   if (it == cache.end()) {
     std::vector<int4> tl = make_tiles(n, 1);
     ElemTiles e;
     int rc = upload(tl, &e.dev);
     if (rc) return rc;
     e.count = (int)tl.size();
-    it = cache.emplace(n, e).first;
+    it = cache.emplace(key, e).first;
   }
   *tiles = it->second.dev;
   *count = it->second.count;
@@ -228,17 +338,26 @@ static bool tables_match(const int64_t *sched, int64_t nsched, const int64_t *su
 // Volume Gauss-Seidel of all elements: cpt co-resident CTAs per element
 // (cooperative launch, grid barrier per hyperplane) when the device can hold
 // at least two per element, else one CTA per element (block barrier).
+// co-resident CTAs of a kernel on the current device (cached per device)
+template <class K>
+static int device_capacity(K kern, int threads, std::map<int, int> &cache) {
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  const int dev = current_device();
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, threads, 0);
+  const int cap = sms * (per > 0 ? per : 1);
+  cache.emplace(dev, cap);
+  return cap;
+}
+
 template <int VAR>
 static int launch_gs_volume(GSDesc G, cudaStream_t st) {
-  static int capacity = 0;
-  if (capacity == 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gs_volume_kernel<VAR, true>,
-                                                  gs_volume_threads<VAR, true>(), 0);
-    capacity = sms * (per > 0 ? per : 1);
-  }
+  static std::map<int, int> caps;
+  const int capacity = device_capacity(gs_volume_kernel<VAR, true>,
+                                       gs_volume_threads<VAR, true>(), caps);
   // enough CTAs per element to give each thread about one point per
   // hyperplane, within the co-residency limit; the grid barrier (~2 us per
   // hyperplane) and L1-bypassing loads do not pay for narrow hyperplanes
@@ -253,6 +372,7 @@ static int launch_gs_volume(GSDesc G, cudaStream_t st) {
   }
   G.cpt = cpt;
   void *args[] = {(void *)&G};
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaLaunchCooperativeKernel((void *)gs_volume_kernel<VAR, true>,
                                               G.ntets * cpt, TC, args, 0, st);
   if (e != cudaSuccess) {
@@ -287,13 +407,14 @@ int hhg_apply_nodal_3d(int64_t n, const int64_t *, const double *v, const double
   return dispatch_volume<SRC_LATTICE>(D, HHG_VAR_NODAL, 0, S(stream));
 }
 
-int hhg_apply_const_3d(int64_t n, const int64_t *, const double *v, const double *s15,
-                       double, double *out, void *stream) {
+int hhg_apply_const_3d(int64_t n, const int64_t *, const double *v, const double *s,
+                       double c0, double *out, void *stream) {
   if (n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
-  // s15: 14 neighbour weights followed by c0 (device); the c0 argument is
-  // accepted for signature parity and must equal s15[14]
+  // s: the 14 neighbour weights (device), c0: the diagonal weight (by value),
+  // exactly kernels.apply_const_3d(n, base, v, s, c0, out)
   if (n < 4) return HHG_OK;
-  VolDesc D = elem_desc(n, v, v, s15, 15, out);
+  VolDesc D = elem_desc(n, v, v, s, 14, out);
+  D.c0 = c0;
   int rc = elem_tiles((int)n, &D.tiles, &D.ntiles);
   if (rc) return rc;
   return dispatch_volume<SRC_LATTICE>(D, HHG_VAR_CONST, 0, S(stream));
@@ -316,8 +437,10 @@ struct Hyperplanes {
 };
 
 static int hyperplanes(int n, const int **ptr, const int **code) {
-  static std::map<int, Hyperplanes> cache;
-  auto it = cache.find(n);
+  static std::map<std::pair<int, int>, Hyperplanes> cache;
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  const auto key = std::make_pair(current_device(), n);
+  auto it = cache.find(key);
   if (it == cache.end()) {
     const int hmin = 6, hmax = 3 * n - 6;
     std::vector<int> p(std::max(hmax - hmin + 2, 1), 0), c;
@@ -334,7 +457,7 @@ static int hyperplanes(int n, const int **ptr, const int **code) {
     int rc = upload(p, &hp.ptr);
     if (!rc) rc = upload(c, &hp.code);
     if (rc) return rc;
-    it = cache.emplace(n, hp).first;
+    it = cache.emplace(key, hp).first;
   }
   *ptr = it->second.ptr;
   *code = it->second.code;
@@ -362,6 +485,18 @@ static int gs_elem(int var, int64_t n, double *u, const double *fv, const double
   if (var == 0) gs_volume_kernel<0, false><<<1, gs_volume_threads<0, false>(), 0, st>>>(G);
   else gs_volume_kernel<1, false><<<1, gs_volume_threads<1, false>(), 0, st>>>(G);
   return check("gs_volume_kernel");
+}
+
+int hhg_csr_gs(int64_t nrows_list, const int64_t *rows, const int64_t *indptr,
+               const int64_t *indices, const double *data, const double *diag, double *u,
+               const double *f, double omega, void *stream) {
+  if (nrows_list <= 0) return HHG_OK;
+  if (!rows || !indptr || !indices || !data || !diag || !u || !f) return HHG_ERR_ARG;
+  csr_gs_kernel<<<1, 32, 0, S(stream)>>>(
+      nrows_list, reinterpret_cast<const long long *>(rows),
+      reinterpret_cast<const long long *>(indptr), reinterpret_cast<const long long *>(indices),
+      data, diag, u, f, omega);
+  return check("csr_gs_kernel");
 }
 
 int hhg_gs_scaling_3d(int64_t n, const int64_t *, double *u, const double *fv,
@@ -397,6 +532,7 @@ static VolDesc grid_desc(const hhg_grid *g) {
   D.ntiles = g->ntiles;
   D.mtiles = reinterpret_cast<const int4 *>(g->mtiles);
   D.nmtiles = g->nmtiles;
+  D.n_nodes = g->n_nodes;
   return D;
 }
 
@@ -551,10 +687,13 @@ int hhg_p2p_pull(double *out, const int64_t *ids, int64_t count, const double *r
                  int *err, void *stream) {
   if (count <= 0) return HHG_OK;
   if (!out || !ids || !recv || !flag || !err) return HHG_ERR_ARG;
+  p2p_wait_kernel<<<1, 32, 0, S(stream)>>>(flag, target, err);
+  int rc = check("p2p_wait_kernel");
+  if (rc) return rc;
   const int blocks = (int)std::min<int64_t>((count + 255) / 256, 64);
-  p2p_pull_kernel<<<blocks, 256, 0, S(stream)>>>(out, reinterpret_cast<const long long *>(ids),
-                                                count, recv, flag, target, recv_first, err);
-  return check("p2p_pull_kernel");
+  p2p_add_kernel<<<blocks, 256, 0, S(stream)>>>(out, reinterpret_cast<const long long *>(ids),
+                                                count, recv, recv_first, err);
+  return check("p2p_add_kernel");
 }
 
 int hhg_device_alloc(int64_t bytes, void **ptr) {
@@ -639,14 +778,8 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_su
   G.ent_col = gs->ent_col;
   G.ent_val = gs->ent_val;
   G.row_diag = gs->row_diag;
-  static int max_blocks = 0;
-  if (max_blocks == 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gs_surface_all_kernel, 64, 0);
-    max_blocks = sms * (per > 0 ? per : 1);
-  }
+  static std::map<int, int> caps;
+  const int max_blocks = device_capacity(gs_surface_all_kernel, 64, caps);
   // spread each level over many SMs (a single SM's outstanding-miss limit
   // bounds a level to ~15 us); ~8 rows per 64-thread block
   long long width = (s->nrows + gs->nlev - 1) / gs->nlev;
@@ -656,6 +789,7 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_su
   const long long *lp = reinterpret_cast<const long long *>(gs->level_ptr);
   int nl = (int)gs->nlev;
   void *args[] = {(void *)&G, (void *)&lp, (void *)&nl};
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaLaunchCooperativeKernel((void *)gs_surface_all_kernel, blocks, 64, args,
                                               0, S(stream));
   if (e != cudaSuccess) {
@@ -698,18 +832,11 @@ int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double
 
 template <bool NODAL, bool AOS>
 static int ten_smem_ok() {
-  static bool done = false;
-  if (!done) {
-    const int smem = (int)ten_smem<NODAL>(ten_threads<NODAL>());
-    if (cudaFuncSetAttribute(tensor_volume_kernel<NODAL, false, AOS>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ||
-        cudaFuncSetAttribute(tensor_volume_kernel<NODAL, true, AOS>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ||
-        cudaFuncSetAttribute(tensor_gs_kernel<NODAL, AOS>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
-      return HHG_ERR_CUDA;
-    done = true;
-  }
+  const int smem = (int)ten_smem<NODAL>(ten_threads<NODAL>());
+  if (smem_optin((const void *)tensor_volume_kernel<NODAL, false, AOS>, smem) ||
+      smem_optin((const void *)tensor_volume_kernel<NODAL, true, AOS>, smem) ||
+      smem_optin((const void *)tensor_gs_kernel<NODAL, AOS>, smem))
+    return HHG_ERR_CUDA;
   return HHG_OK;
 }
 
@@ -722,8 +849,9 @@ struct TenTiles {
 };
 
 static int tensor_tiles(int n, int ntets, int tr, TenTiles &out) {
-  static std::map<std::tuple<int, int, int>, TenTiles> cache;
-  const auto key = std::make_tuple(n, ntets, tr);
+  static std::map<std::tuple<int, int, int, int>, TenTiles> cache;
+  std::lock_guard<std::mutex> lock(g_cache_mu);
+  const auto key = std::make_tuple(current_device(), n, ntets, tr);
   auto it = cache.find(key);
   if (it == cache.end()) {
     std::vector<int4> tl;
@@ -745,18 +873,12 @@ static int tensor_tiles(int n, int ntets, int tr, TenTiles &out) {
 template <bool NODAL>
 static int ten_tile_apply(const TenDesc &D, bool res, cudaStream_t st) {
   TenTiles cache;
-  static bool configured = false;
   int rc = tensor_tiles(D.n, D.ntets, tt_rows<NODAL>(), cache);
   if (rc) return rc;
   const int smem = (int)tt_smem<NODAL>();
-  if (!configured) {
-    if (cudaFuncSetAttribute(tensor_tile_kernel<NODAL, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem) ||
-        cudaFuncSetAttribute(tensor_tile_kernel<NODAL, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem))
-      return HHG_ERR_CUDA;
-    configured = true;
-  }
+  if (smem_optin((const void *)tensor_tile_kernel<NODAL, false>, smem) ||
+      smem_optin((const void *)tensor_tile_kernel<NODAL, true>, smem))
+    return HHG_ERR_CUDA;
   if (cache.count == 0) return HHG_OK;
   if (res)
     tensor_tile_kernel<NODAL, true><<<cache.count, tt_threads<NODAL>(), smem, st>>>(D, cache.dev);
@@ -935,6 +1057,8 @@ int hhg_tensor_surface_prepare(const hhg_grid *g, const hhg_surface *s,
   tensor_surface_fill_kernel<<<(int)((s->nrows + 127) / 128), 128, 0, S(stream)>>>(G, km);
   return check("tensor_surface_fill_kernel");
 }
+
+long long hhg_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 int hhg_status(void) {
   int v = 0;

@@ -421,35 +421,80 @@ __global__ void p2p_signal_kernel(unsigned long long *remote_flag) {
   atomicAdd_system(remote_flag, 1ULL);
 }
 
-// wait until the neighbour's push of this apply has arrived (its counter
-// reaches `target`; bounded spin, *err set on timeout), then complete the
-// interface rows in rank order: out = recv + mine if recv_first else
-// mine + recv (bitwise the NCCL path's sum on both ranks)
-__global__ void p2p_pull_kernel(double *out, const long long *ids, long long count,
-                                const double *recv, const unsigned long long *flag,
-                                unsigned long long target, int recv_first, int *err) {
-  __shared__ int ok;
-  if (threadIdx.x == 0) {
-    unsigned long long v = 0;
-    long long spins = 0;
-    for (;;) {
-      asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-      if (v >= target) break;
-      if (++spins > (1LL << 30)) break;          // ~a minute: never hang the GPU
-      __nanosleep(64);
-    }
-    ok = v >= target;
-    if (!ok) atomicExch(err, 1);
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
+// wait until the neighbour's push of this apply has arrived: one thread of
+// one CTA spins (bounded, *err set on timeout) so no spinning CTA takes SM
+// slots from the volume kernel running concurrently; the adds follow as a
+// separate, non-spinning launch on the same stream (p2p_add_kernel)
+__global__ void p2p_wait_kernel(const unsigned long long *flag, unsigned long long target,
+                                int *err) {
+  if (threadIdx.x != 0) return;
+  unsigned long long v = 0;
+  long long spins = 0;
+  for (;;) {
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+    if (v >= target) break;
+    if (++spins > (1LL << 30)) break;          // ~a minute: never hang the GPU
+    __nanosleep(64);
   }
-  __syncthreads();
-  if (!ok) return;
+  if (v < target) atomicExch(err, 1);
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+
+// complete the interface rows in rank order: out = recv + mine if
+// recv_first else mine + recv (bitwise the NCCL path's sum on both ranks);
+// skipped after a timeout
+__global__ void p2p_add_kernel(double *out, const long long *ids, long long count,
+                               const double *recv, int recv_first, const int *err) {
+  if (*((volatile const int *)err)) return;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count;
        i += (long long)gridDim.x * blockDim.x) {
     const long long g = ids[i];
     const double theirs = __ldcv(recv + i);
     const double mine = out[g];
     out[g] = recv_first ? dadd(theirs, mine) : dadd(mine, theirs);
+  }
+}
+
+// kernels.csr_gs (kernels.py:979-992): forward Gauss-Seidel over the given
+// rows of a CSR matrix, strictly in list order, bitwise the sequential loop
+// (acc += data * u[col] in stored order, diagonal skipped).  One warp: the
+// lanes load and multiply a row's entries 32 at a time, lane 0 adds the
+// products in order; a zero diagonal stops the sweep at that row and sets
+// the status word (the reference raises there).
+__global__ void csr_gs_kernel(long long nr, const long long *rows, const long long *indptr,
+                              const long long *indices, const double *data, const double *diag,
+                              double *u, const double *f, double omega) {
+  const int lane = threadIdx.x;
+  for (long long ri = 0; ri < nr; ++ri) {
+    const long long r = rows[ri];
+    const long long e0 = indptr[r], e1 = indptr[r + 1];
+    double acc = 0.0;
+    for (long long b = e0; b < e1; b += 32) {
+      const long long e = b + lane;
+      double prod = 0.0;
+      bool use = false;
+      if (e < e1) {
+        const long long c = indices[e];
+        use = c != r;
+        if (use) prod = dmul(data[e], __ldcv(u + c));
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, use);
+      const int cnt = (int)min(32LL, e1 - b);
+      for (int x = 0; x < cnt; ++x) {
+        const double px = __shfl_sync(0xffffffffu, prod, x);
+        if (lane == 0 && (m >> x & 1)) acc = dadd(acc, px);
+      }
+    }
+    const double d0 = diag[r];
+    if (d0 == 0.0) {
+      if (lane == 0) atomicOr(&g_status, 1);
+      return;
+    }
+    if (lane == 0)
+      __stcg(u + r, dadd(dmul(dsub(1.0, omega), __ldcv(u + r)),
+                         ddiv(dmul(omega, dsub(f[r], acc)), d0)));
+    __syncwarp();
+    __threadfence_block();
   }
 }
 

@@ -95,22 +95,23 @@ int hhg_dot(int64_t n, const double *x, const double *y, double *work, double *r
   if (nb > hhg::DOT_BLOCKS) nb = hhg::DOT_BLOCKS;
   if (nb < 1) nb = 1;
   hhg::dot_partial<<<nb, 256, 0, st>>>(n, x, y, work);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   hhg::dot_final<<<1, 1024, 0, st>>>(nb, work, result);
-  return cudaGetLastError() == cudaSuccess ? HHG_OK : HHG_ERR_CUDA;
+  return check("dot");
 }
 
 int hhg_axpy_ratio(int64_t n, const double *num, const double *den, double sign,
                    const double *x, double *y, void *stream) {
   hhg::axpy_ratio_kernel<<<vec_grid(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       n, num, den, sign, x, y);
-  return cudaGetLastError() == cudaSuccess ? HHG_OK : HHG_ERR_CUDA;
+  return check("vector kernel");
 }
 
 int hhg_xpay_ratio(int64_t n, const double *num, const double *den, const double *r,
                    double *p, void *stream) {
   hhg::xpay_ratio_kernel<<<vec_grid(n), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
       n, num, den, r, p);
-  return cudaGetLastError() == cudaSuccess ? HHG_OK : HHG_ERR_CUDA;
+  return check("vector kernel");
 }
 
 int hhg_csr_spmv(int64_t nrows, const int64_t *indptr, const int64_t *indices,
@@ -121,7 +122,7 @@ int hhg_csr_spmv(int64_t nrows, const int64_t *indptr, const int64_t *indices,
                          reinterpret_cast<cudaStream_t>(stream)>>>(
       nrows, reinterpret_cast<const long long *>(indptr),
       reinterpret_cast<const long long *>(indices), data, x, y, accumulate);
-  return cudaGetLastError() == cudaSuccess ? HHG_OK : HHG_ERR_CUDA;
+  return check("vector kernel");
 }
 
 int hhg_scatter_zero(int64_t n, const int64_t *ids, double *y, void *stream) {
@@ -129,7 +130,7 @@ int hhg_scatter_zero(int64_t n, const int64_t *ids, double *y, void *stream) {
   hhg::scatter_zero_kernel<<<(int)((n + 255) / 256), 256, 0,
                              reinterpret_cast<cudaStream_t>(stream)>>>(
       n, reinterpret_cast<const long long *>(ids), y);
-  return cudaGetLastError() == cudaSuccess ? HHG_OK : HHG_ERR_CUDA;
+  return check("vector kernel");
 }
 
 }  // extern "C"

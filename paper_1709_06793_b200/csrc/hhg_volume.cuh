@@ -28,6 +28,7 @@ constexpr int VOL_COLS = 34;  // 32 lanes + halo
 struct VolDesc {
   int n, ntets;
   long long L, nvol, S;
+  long long n_nodes;           // length of the global vectors (SPLIT)
   const long long *vol_start;  // global layout: first volume id per tet
   const int *srow;             // shell row offsets (host checks; kernels use srow32)
   const double *ghost;         // [ntets*S]
@@ -37,6 +38,7 @@ struct VolDesc {
   double *out;                 // global vector or [ntets*nvol]
   const double *coef;          // per-tet coefficients (sh, fac, const)
   int coef_stride;
+  double c0;                   // const variant, coef_stride 14: diagonal weight
   const double *w;             // stored stencils [ntets*nvol*15]
   const int4 *tiles;
   int ntiles;
@@ -354,7 +356,9 @@ struct RowOp<2, FAST> {  // constant coefficient: c0 v0 + sum s_d v_q
   double s[15];
   __device__ void init(const VolDesc &D, int t, double *) {
 #pragma unroll
-    for (int d = 0; d < 15; ++d) s[d] = __ldg(D.coef + (long long)t * D.coef_stride + d);
+    for (int d = 0; d < 14; ++d) s[d] = __ldg(D.coef + (long long)t * D.coef_stride + d);
+    // batched path: 15 weights per element; per-element ABI: 14 + c0 by value
+    s[14] = D.coef_stride == 15 ? __ldg(D.coef + (long long)t * 15 + 14) : D.c0;
   }
   __device__ __forceinline__ double operator()(double v0, double, const double2 (&q)[14],
                                                int) const {
@@ -620,9 +624,86 @@ __device__ __forceinline__ void mirror_step(const Win<B> &mi, const Win<B> &hi,
   c.t5 = edge_term<B>(hi.C[B], mi.C[B + 1], sh[5]);
 }
 
+// --------------------------------------------------------------------------
+// FMA edge-flux step.  P[s] carries the pre-summed down-plane terms
+// (0,0,-1), (1,0,-1), (-1,1,-1), (0,1,-1) of row s of plane kk; the step
+// finishes the rows of plane kk from windows mi (kk) and hi (kk+1) and
+// leaves P for plane kk+1.  sh[d] == sh[d+7] (host-checked): the terms of
+// an edge seen from its two ends are negatives of each other.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ double fterm(double2 p, double2 q, double sh, double acc) {
+  return fma((p.y + q.y) * sh, q.x - p.x, acc);
+}
+__device__ __forceinline__ double fflux(double2 p, double2 q, double sh) {
+  return ((p.y + q.y) * sh) * (q.x - p.x);
+}
+// sh * [(k0+ka)(va-v0) + (k0+kb)(vb-v0)] + acc
+__device__ __forceinline__ double fpair(double2 p, double2 a, double2 b, double sh, double acc) {
+  double m = (p.y + a.y) * (a.x - p.x);
+  m = fma(p.y + b.y, b.x - p.x, m);
+  return fma(sh, m, acc);
+}
+
+template <int B>
+__device__ __forceinline__ void fma_seed(const Win<B> &lo, const Win<B> &mi,
+                                        const double (&sh)[7], double (&P)[B]) {
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const double2 c = mi.C[s + 1];
+    double a = fflux(c, lo.C[s + 1], sh[2]);                 // (0,0,-1)
+    a = fterm(c, lo.R[s + 1], sh[4], a);                     // (1,0,-1)
+    a = fterm(c, lo.L[s + 1], sh[6], a);                     // (-1,1,-1)
+    a = fterm(c, lo.C[s + 2], sh[5], a);                     // (0,1,-1)
+    P[s] = a;
+  }
+}
+
+template <int B>
+__device__ __forceinline__ void fma_step(const Win<B> &mi, const Win<B> &hi,
+                                        const double (&sh)[7], double (&P)[B],
+                                        double (&out)[B]) {
+  double Pn[B], F1[B];
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const double2 p = mi.C[s + 1];
+    double acc = P[s];
+    acc = fpair(p, mi.R[s + 1], mi.L[s], sh[0], acc);        // (1,0,0) (-1,0,0)
+    acc = fpair(p, mi.R[s], mi.L[s + 1], sh[3], acc);        // (1,-1,0) (-1,1,0)
+    if (s + 1 < B) {                                         // (0,1,0), shared with s+1
+      F1[s] = fflux(p, mi.C[s + 2], sh[1]);
+      acc += F1[s];
+    } else {
+      acc = fterm(p, mi.C[s + 2], sh[1], acc);
+    }
+    acc = (s >= 1) ? acc - F1[s - 1] : fterm(p, mi.C[s], sh[1], acc);   // (0,-1,0)
+    const double F2 = fflux(p, hi.C[s + 1], sh[2]);          // (0,0,1), shared with kk+1
+    acc += F2;
+    Pn[s] = -F2;
+    acc = fterm(p, hi.R[s], sh[6], acc);                     // (1,-1,1)
+    acc = fterm(p, hi.L[s], sh[4], acc);                     // (-1,0,1)
+    if (s >= 1) {                                            // (0,-1,1), shared with
+      const double F12 = fflux(p, hi.C[s], sh[5]);           // (0,1,-1) of row s-1 at kk+1
+      acc += F12;
+      Pn[s - 1] -= F12;
+    } else {
+      acc = fterm(p, hi.C[s], sh[5], acc);
+    }
+    out[s] = acc;
+  }
+#pragma unroll
+  for (int s = 0; s < B; ++s) {
+    const double2 c = hi.C[s + 1];
+    double a = fterm(c, mi.R[s + 1], sh[4], Pn[s]);          // (1,0,-1)
+    a = fterm(c, mi.L[s + 1], sh[6], a);                     // (-1,1,-1)
+    if (s == B - 1) a = fterm(c, mi.C[B + 1], sh[5], a);     // (0,1,-1), last row
+    P[s] = a;
+  }
+}
+
 // NW warps per CTA, each 8 columns x 4B rows (8x4 lanes, B rows per lane):
 // a tile is 8*NW columns x 4B rows of one element, marching in k
-template <int SRC, bool RES, int B, int NS, int MINB, int NW>
+// MODE 0: bitwise reference order (mirror_step); MODE 1: FMA edge-flux form
+template <int SRC, bool RES, int B, int NS, int MINB, int NW, int MODE = 0>
 __global__ void __launch_bounds__(32 * NW, MINB)
 volume_kernel_mirror(VolDesc D) {
   constexpr int ROWS = 4 * B + 2;
@@ -743,7 +824,8 @@ volume_kernel_mirror(VolDesc D) {
   }
 
   Win<B> X0, X1, X2;
-  MirrorCarry<B> carry;
+  MirrorCarry<B> carry;   // MODE 0
+  double P[B];            // MODE 1
 
   // fetch plane q into window w, release its slot, refill PD planes ahead
   auto fetch = [&](int q, Win<B> &w) {
@@ -779,8 +861,10 @@ volume_kernel_mirror(VolDesc D) {
       if constexpr (HHG_VOL_EXPT == 1) {          // data movement only
 #pragma unroll
         for (int s = 0; s < B; ++s) vals[s] = hi.C[s + 1].x + mi.R[s].y + mi.L[s + 1].x;
-      } else {
+      } else if constexpr (MODE == 0) {
         mirror_step<B>(mi, hi, sh, carry, vals);
+      } else {
+        fma_step<B>(mi, hi, sh, P, vals);
       }
       emit(q - 1, vals);
     }
@@ -789,7 +873,10 @@ volume_kernel_mirror(VolDesc D) {
   if (kmax >= 1) {
     fetch(0, X0);
     fetch(1, X1);
-    if (warp_min_ij <= n - 2) mirror_seed<B>(X0, X1, sh, carry);
+    if (warp_min_ij <= n - 2) {
+      if constexpr (MODE == 0) mirror_seed<B>(X0, X1, sh, carry);
+      else fma_seed<B>(X0, X1, sh, P);
+    }
     step(2, X1, X2);
     for (int q = 3; q <= kmax + 1; q += 3) {
       step(q, X2, X0);

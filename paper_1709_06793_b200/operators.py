@@ -241,10 +241,14 @@ class Operator:
         f = _lib.FLAG_RESIDUAL if residual else 0
         if self.is_tensor and self._stored is None:
             return f
+        # mirror-symmetric stencils: edge terms shared by two rows of a thread
+        # are evaluated once (bitwise); with fast=True the FMA edge-flux form
+        # of the same kernel (hhg_volume.cuh fma_step, <= 1e-12 of the
+        # reference order)
+        if self._mirror and self._vol_variant() == _lib.VAR["scaling"]:
+            f |= _lib.FLAG_MIRROR
         if self.fast and self.variant != "nodal":
             f |= _lib.FLAG_FAST
-        elif self._mirror and self._vol_variant() == _lib.VAR["scaling"]:
-            f |= _lib.FLAG_MIRROR
         return f
 
     def _vol_variant(self):
@@ -256,7 +260,7 @@ class Operator:
             return _lib.VAR["const"]
         return _lib.VAR["scaling"]
 
-    def _to_dev(self, x, name="grid function", pipelined=False):
+    def _to_dev(self, x, name="grid function"):
         """(device tensor, kind) with kind 'cuda' (device input, no copy),
         'host' (CPU torch tensor: pinned-friendly non-blocking copy) or
         'numpy' (reference contract: numpy in, numpy out)."""
@@ -267,8 +271,6 @@ class Operator:
                 raise ValueError(f"{name} has wrong length")
             if x.is_cuda:
                 return x.to(dtype=torch.float64).contiguous(), "cuda"
-            if pipelined and x.dtype == torch.float64 and x.is_contiguous():
-                return x, "host-pipe"
             return x.to(device="cuda", dtype=torch.float64, non_blocking=True), "host"
         a = np.asarray(x, dtype=np.float64)
         if a.shape != (self.grid.n_nodes,):
@@ -399,83 +401,185 @@ class Operator:
                 "streams": [torch.cuda.Stream() for _ in range(3)],
                 "du": torch.empty(n, dtype=torch.float64, device="cuda"),
                 "out": torch.empty(n, dtype=torch.float64, device="cuda"),
-                "host_out": torch.empty(n, dtype=torch.float64, pin_memory=True),
                 "byref": ctypes.byref,
             }
         return self._pipe
 
-    def apply_host(self, u_host):
-        """A u for a (pinned) CPU tensor, H2D / kernels / D2H overlapped per
-        group of macro elements: the surface block goes first (the ghost
+    def _chunks(self):
+        """Host<->device copy ranges of the pipeline: the surface block, then
+        one contiguous volume block per group of macro elements."""
+        P = self._pipeline()
+        grid = self.grid
+        ns, vs, nv = grid.n_surface_nodes, grid.vol_start, grid.nodes_per_volume
+        out = [(0, ns)]
+        for g in range(len(P["descs"])):
+            if nv:
+                out.append((int(vs[P["bounds"][g]]), int(vs[P["bounds"][g + 1] - 1] + nv)))
+            else:
+                out.append((ns, ns))
+        return out
+
+    def _staging(self, key):
+        """Persistent pinned staging vector (numpy inputs of apply_host)."""
+        P = self._pipeline()
+        if key not in P:
+            torch = self._device()["torch"]
+            P[key] = torch.empty(self.grid.n_nodes, dtype=torch.float64, pin_memory=True)
+        return P[key]
+
+    def apply_host(self, u_host, f_host=None):
+        """A u (or f - A u) for host inputs, H2D / kernels / D2H overlapped
+        per group of macro elements: the surface block goes first (the ghost
         update needs only surface values), each group's volume block is
         applied as soon as it has landed and copied back while the next
         group is in flight; the surface rows (which read interior values of
-        every element) run last.  Returns a pinned CPU tensor."""
+        every element) run last.
+
+        Inputs are pinned CPU float64 tensors, or numpy arrays: those are
+        copied chunk by chunk into persistent pinned staging buffers by a
+        pool of host threads, each chunk's H2D enqueued as soon as its copy
+        is done.  Returns a fresh pinned CPU tensor (a numpy view of one for
+        numpy inputs)."""
         D = self._device()
         torch = D["torch"]
         P = self._pipeline()
         grid, dg, ds = self.grid, D["grid"], D["surf"]
         h2d, comp, d2h = P["streams"]
-        du, out, hout = P["du"], P["out"], P["host_out"]
-        ns = grid.n_surface_nodes
-        vs = grid.vol_start
-        nv = grid.nodes_per_volume
-        flags = self._vol_flags()
+        du, out = P["du"], P["out"]
+        res = f_host is not None
+        df = None
+        if res:
+            if "df" not in P:
+                P["df"] = torch.empty_like(du)
+            df = P["df"]
+        numpy_in = isinstance(u_host, np.ndarray)
+        srcs = [(u_host, du, "stage_u")] + ([(f_host, df, "stage_f")] if res else [])
+        # a fresh pinned result per call (the reference returns a new array;
+        # torch's caching host allocator recycles freed blocks)
+        hout = torch.empty(grid.n_nodes, dtype=torch.float64, pin_memory=True)
+        chunks = self._chunks()
+        flags = self._vol_flags(residual=res)
         wp = D["w"].data_ptr() if D["w"] is not None else None
         if self.surface_mode == "csr":
             ds.csr(dg)          # one-time fill on this stream, before the others join it
         cur = torch.cuda.current_stream()
         for st in P["streams"]:
             st.wait_stream(cur)
+        pending = {}
+        if numpy_in:
+            pool = P.get("pool")
+            if pool is None:
+                import os
+                from concurrent.futures import ThreadPoolExecutor
+                pool = P["pool"] = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+            views = [(src, self._staging(key).numpy()) for src, _, key in srcs]
+            for ci, (a, b) in enumerate(chunks):
+                if b > a:
+                    pending[ci] = [pool.submit(np.copyto, stg[a:b], src[a:b])
+                                   for src, stg in views]
         ev_in = []
         with torch.cuda.stream(h2d):
-            du[:ns].copy_(u_host[:ns], non_blocking=True)
-            e = torch.cuda.Event()
-            e.record(h2d)
-            ev_in.append(e)
-            for g in range(len(P["descs"])):
-                a, b = int(vs[P["bounds"][g]]) if nv else ns, \
-                    int(vs[P["bounds"][g + 1] - 1] + nv) if nv else ns
+            for ci, (a, b) in enumerate(chunks):
                 if b > a:
-                    du[a:b].copy_(u_host[a:b], non_blocking=True)
+                    for fut in pending.get(ci, ()):
+                        fut.result()
+                    for src, dst, key in srcs:
+                        host = self._staging(key) if numpy_in else src
+                        dst[a:b].copy_(host[a:b], non_blocking=True)
                 e = torch.cuda.Event()
                 e.record(h2d)
                 ev_in.append(e)
         comp.wait_event(ev_in[0])
         cs = comp.cuda_stream
+        fp = df.data_ptr() if res else None
         check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), cs), "ghost_update")
         for g, desc in enumerate(P["descs"]):
             comp.wait_event(ev_in[g + 1])
             check(lib.hhg_volume_apply(P["byref"](desc), self._vol_variant(), flags,
-                                       D["coef"].data_ptr(), wp, du.data_ptr(), None,
+                                       D["coef"].data_ptr(), wp, du.data_ptr(), fp,
                                        out.data_ptr(), cs), "volume_apply")
             e = torch.cuda.Event()
             e.record(comp)
             d2h.wait_event(e)
-            if nv:
-                a, b = int(vs[P["bounds"][g]]), int(vs[P["bounds"][g + 1] - 1] + nv)
+            a, b = chunks[g + 1]
+            if b > a:
                 with torch.cuda.stream(d2h):
                     hout[a:b].copy_(out[a:b], non_blocking=True)
-        self._surface(dg, ds, 0, du, None, out, cs)
+        self._surface(dg, ds, flags & _lib.FLAG_RESIDUAL, du, fp, out, cs)
         e = torch.cuda.Event()
         e.record(comp)
         d2h.wait_event(e)
+        a, b = chunks[0]
         with torch.cuda.stream(d2h):
-            hout[:ns].copy_(out[:ns], non_blocking=True)
+            hout[a:b].copy_(out[a:b], non_blocking=True)
         d2h.synchronize()
         self._count()
-        return hout
+        return hout.numpy() if numpy_in else hout
+
+    @property
+    def _S(self):
+        """The surface rows as the reference's scipy CSR matrix
+        (``Operator._S``, operators.py:329-365: n_nodes x n_nodes, rows of the
+        free surface nodes only, duplicates summed).  Built once, lazily, from
+        the rows the device filled for apply / smooth (neighbour ids and
+        weights per incidence and direction, diagonal = minus their sum); the
+        values are the reference's up to summation order (<= 1e-13)."""
+        if getattr(self, "_S_cache", None) is None:
+            import scipy.sparse as sp
+            D = self._device()
+            torch = D["torch"]
+            dg, ds = D["grid"], D["surf"]
+            c = ds.csr(dg)
+            torch.cuda.synchronize()
+            rows = np.asarray(ds.st.rows, dtype=np.int64)
+            nr = len(rows)
+            ptr = c["keep"][0].cpu().numpy()
+            nent = int(ptr[-1]) if nr else 0
+            col = c["keep"][1].cpu().numpy()[:nent].astype(np.int64)
+            val = c["keep"][2].cpu().numpy()[:nent]
+            diag = c["keep"][3].cpu().numpy()[:nr]
+            r = np.repeat(rows, np.diff(ptr))
+            n = self.grid.n_nodes
+            S = sp.coo_matrix((np.concatenate([val, diag]),
+                               (np.concatenate([r, rows]), np.concatenate([col, rows]))),
+                              shape=(n, n)).tocsr()
+            S.sum_duplicates()
+            self._S_cache = S
+        return self._S_cache
 
     # -- public operations (reference signatures) ------------------------------
+    def _host_input(self, x, name):
+        """x as an input of the host pipeline (float64 numpy array or pinned-
+        friendly contiguous CPU float64 tensor), or None if it is not one."""
+        if self.is_tensor:
+            return None
+        torch = self._device()["torch"]
+        if isinstance(x, torch.Tensor):
+            if x.is_cuda or x.dtype != torch.float64 or not x.is_contiguous():
+                return None
+            if x.shape != (self.grid.n_nodes,):
+                raise ValueError(f"{name} has wrong length")
+            return x
+        a = np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+        if a.shape != (self.grid.n_nodes,):
+            raise ValueError(f"{name} has wrong length")
+        return a
+
     def apply(self, u):
         """Matrix action A u with identity on Dirichlet rows."""
-        du, kind = self._to_dev(u, pipelined=not self.is_tensor)
-        if kind == "host-pipe":
-            return self.apply_host(du)
+        h = self._host_input(u, "grid function")
+        if h is not None:
+            return self.apply_host(h)
+        du, kind = self._to_dev(u)
         return self._from_dev(self.apply_device(du), kind)
 
     def residual(self, u, f):
         """r = f - A u, forced to zero on Dirichlet rows."""
+        hu = self._host_input(u, "grid function")
+        hf = self._host_input(f, "right-hand side") if hu is not None else None
+        if hu is not None and hf is not None and isinstance(hu, np.ndarray) == \
+                isinstance(hf, np.ndarray):
+            return self.apply_host(hu, hf)
         du, kind = self._to_dev(u)
         df, _ = self._to_dev(f, "right-hand side")
         return self._from_dev(self.apply_device(du, f=df), kind)

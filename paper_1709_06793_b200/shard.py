@@ -129,6 +129,9 @@ class PeerExchange:
 
     def __init__(self, op, imap: InterfaceMap):
         import torch
+        if getattr(op, "surface_mode", "csr") != "csr":
+            # the pushes are stored by the precomputed-row surface kernel only
+            raise ValueError("peer exchange needs surface_mode='csr'")
         self.torch, self.op, self.imap = torch, op, imap
         self.rank = imap.rank
         D = op._device()
@@ -323,6 +326,11 @@ class ShardedOperator:
         out = torch.from_numpy(np.asarray(self.op.apply(u.numpy()), dtype=np.float64))
         return exchange_partials(out, self.imap, self.dist, self._index(out.device))
 
+    def check(self):
+        """Raise if a peer-memory exchange timed out (call after a host sync)."""
+        if self.peer is not None:
+            self.peer.check()
+
     def residual(self, u, f):
         """f - A u, zero on Dirichlet rows."""
         return (f - self.apply(u)) * self._mask("free", u.device)
@@ -346,6 +354,7 @@ def sharded_cg(sop: ShardedOperator, f, tol=1e-10, max_iter=10000):
     p = r.clone()
     rs = sop.dot(r, r)
     b0 = float(torch.sqrt(rs).item())
+    sop.check()
     if b0 == 0.0:
         return x, 0, 0.0
     it, res = 0, b0
@@ -356,6 +365,7 @@ def sharded_cg(sop: ShardedOperator, f, tol=1e-10, max_iter=10000):
         r = r - alpha * Ap
         rs_new = sop.dot(r, r)
         res = float(torch.sqrt(rs_new).item())
+        sop.check()                       # host sync point: lost peer signals raise
         if res <= tol * b0:
             break
         p = r + (rs_new / rs) * p

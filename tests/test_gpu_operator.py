@@ -58,10 +58,15 @@ def test_element_abi_bitwise(cuda, n):
                                  out.data_ptr(), st))
     assert np.array_equal(out.cpu().numpy(), p("nodal"))
     s = p("s")
-    s15 = _dev(torch, np.append(s, -s.sum()))
-    check(lib.hhg_apply_const_3d(n, None, v.data_ptr(), s15.data_ptr(), -s.sum(),
+    s14 = _dev(torch, np.ascontiguousarray(s))          # 14 weights + c0 by value
+    check(lib.hhg_apply_const_3d(n, None, v.data_ptr(), s14.data_ptr(), -s.sum(),
                                  out.data_ptr(), st))
     assert np.array_equal(out.cpu().numpy(), p("const"))
+    # the c0 argument is the diagonal weight (not read from the array)
+    check(lib.hhg_apply_const_3d(n, None, v.data_ptr(), s14.data_ptr(), 0.0,
+                                 out.data_ptr(), st))
+    assert np.array_equal(out.cpu().numpy(), ok.apply_const_3d(n, M.SimplexLattice(3, n).base,
+                                                               p("v"), s, 0.0))
     w = _dev(torch, p("w"))
     check(lib.hhg_apply_stored_3d(n, None, v.data_ptr(), w.data_ptr(), out.data_ptr(), st))
     assert np.array_equal(out.cpu().numpy(), p("stored"))
@@ -363,6 +368,39 @@ def test_pinned_host_pipeline_equals_device_apply(cuda, name):
     want = op.apply_device(torch.as_tensor(u, device="cuda")).cpu().numpy()
     assert np.array_equal(got.numpy(), want)
     assert np.array_equal(op.apply(u), want)           # numpy in, numpy out
+    # every call returns a fresh buffer (the pinned output was
+    # recycled, so a second apply overwrote the first result)
+    first = op.apply(u)
+    second = op.apply(2.0 * u)
+    assert np.array_equal(first, want)
+    assert np.array_equal(second, op.apply_device(torch.as_tensor(2.0 * u, device="cuda"))
+                          .cpu().numpy())
+    # numpy residual through the same pipeline
+    f = np.random.default_rng(22).uniform(-1, 1, grid.n_nodes)
+    rw = op.apply_device(torch.as_tensor(u, device="cuda"),
+                         f=torch.as_tensor(f, device="cuda")).cpu().numpy()
+    assert np.array_equal(op.residual(u, f), rw)
+    assert np.array_equal(op.residual(host, torch.from_numpy(f).pin_memory()).numpy(), rw)
+
+
+@pytest.mark.parametrize("variant", ["scaling", "nodal", "hybrid:wv"])
+def test_surface_matrix_S_matches_oracle(cuda, variant):
+    """Operator._S (the reference's surface CSR, operators.py:329-365),
+    built from the device-filled rows, equals the independently assembled
+    shell-element matrix entrywise to 1e-13 and reproduces the surface rows
+    of apply."""
+    grid = M.RefinedGrid(case_mesh("c3"), 3)
+    kf = sample_nodal(k_c3(), grid)
+    op = _op(grid, kf, variant)
+    want = CpuOperator(grid, op.variant, kf, hybrid_nodal=op.hybrid_nodal).S.tocsr()
+    S = op._S
+    assert S.shape == (grid.n_nodes, grid.n_nodes)
+    diff = abs(S - want)
+    assert diff.max() <= 1e-13 * abs(want).max()
+    u = np.random.default_rng(5).uniform(-1, 1, grid.n_nodes)
+    rows = np.nonzero(np.diff(S.indptr))[0]
+    assert np.abs(S.dot(u)[rows] - op.apply(u)[rows]).max() <= 1e-13 * np.abs(u).max() * \
+        abs(want).max() * 30
 
 
 def test_constant_field_collapses_variants(cuda):
@@ -404,3 +442,39 @@ def test_every_element_bitwise_against_oracle(cuda, variant, lvl):
         s0 = grid.vol_start[t]
         assert np.array_equal(out[s0:s0 + nvol], want), t
         assert np.array_equal(res[s0:s0 + nvol], f[s0:s0 + nvol] - want), t
+
+
+def test_csr_gs_abi_bitwise(cuda):
+    """hhg_csr_gs against the reference's kernels.csr_gs output (golden)."""
+    torch = cuda
+    g = golden("kernels")
+    import scipy.sparse as sp
+    A = sp.csr_matrix((g["csr_data"], g["csr_indices"], g["csr_indptr"]), shape=(60, 60))
+    d = lambda a, dt=None: torch.as_tensor(np.ascontiguousarray(a, dtype=dt), device="cuda")
+    # device copies kept alive until the kernels have run
+    rows, ptr, idx = (d(g["csr_rows"], np.int64), d(A.indptr, np.int64),
+                      d(A.indices, np.int64))
+    data, diag, f = d(A.data), d(A.diagonal()), d(g["csr_f"])
+    u = d(g["csr_u0"].copy())
+    st = torch.cuda.current_stream().cuda_stream
+    nr = len(g["csr_rows"])
+    check(lib.hhg_csr_gs(nr, rows.data_ptr(), ptr.data_ptr(), idx.data_ptr(), data.data_ptr(),
+                         diag.data_ptr(), u.data_ptr(), f.data_ptr(), 0.9, st))
+    assert np.array_equal(u.cpu().numpy(), g["csr_result"])
+    # a zero diagonal stops the sweep at that row and is reported
+    zd = A.diagonal().copy()
+    zd[g["csr_rows"][3]] = 0.0
+    zdiag = d(zd)
+    u = d(g["csr_u0"].copy())
+    lib.hhg_status_reset()
+    check(lib.hhg_csr_gs(nr, rows.data_ptr(), ptr.data_ptr(), idx.data_ptr(), data.data_ptr(),
+                         zdiag.data_ptr(), u.data_ptr(), f.data_ptr(), 0.9, st))
+    torch.cuda.synchronize()
+    with pytest.raises(ValueError, match="zero central stencil entry"):
+        check(lib.hhg_status())
+    lib.hhg_status_reset()
+    got = u.cpu().numpy()
+    want = g["csr_u0"].copy()
+    rows = g["csr_rows"][:3]
+    ok.csr_gs(rows, A.indptr, A.indices, A.data, A.diagonal(), want, g["csr_f"], 0.9)
+    assert np.array_equal(got, want)
