@@ -222,6 +222,29 @@ def sec_c2_cg():
     save("c2_cg", **out)
 
 
+def sec_norms():
+    """analysis.error_norms (quad=True) of the config-2 manufactured case on
+    a small grid, for a seeded perturbation of the exact interpolant: pins
+    the test harness's restatement of the H1 / quadrature-L2 errors."""
+    from hhgscale import analysis as an
+    import sympy as sy
+    x, y, z = sy.symbols("x y z")
+    u_e = sy.sin(sy.pi * x) * sy.sin(sy.pi * y) * sy.sin(sy.pi * z)
+    k_e = 1 + sy.Rational(1, 2) * sy.exp(-(x ** 2 + y ** 2 + z ** 2))
+    case = an._scalar_case("c2", (x, y, z), u_e, k_e, k_c2(), RM.unit_cube_6,
+                           (np.zeros(3), np.ones(3)), {})
+    out = {}
+    for lvl in (2, 3):
+        g = RM.RefinedGrid(RM.unit_cube_6(), lvl)
+        u = case.u(g.node_coords) + 1e-3 * np.random.default_rng(lvl).normal(size=g.n_nodes)
+        nr = an.error_norms(case, u, g, quad=True)
+        out[f"l{lvl}_u"] = u
+        out[f"l{lvl}_l2"] = nr.l2_quad
+        out[f"l{lvl}_h1"] = nr.h1
+        out[f"l{lvl}_l2d"] = nr.l2_discrete
+    save("norms", **out)
+
+
 def sec_mg_small():
     """Multigrid V-cycles on small grids (fast pins of the solver loop)."""
     from hhgscale.coefficients import catalog
@@ -368,7 +391,7 @@ def sec_coeff():
 
 SECTIONS = {"mesh": sec_mesh, "kernels": sec_kernels, "applies": sec_applies,
             "c3": sec_c3_checksums, "c2": sec_c2_cg, "mg": sec_mg_small, "c4": sec_c4_mg,
-            "tensor": sec_tensor, "coeff": sec_coeff}
+            "tensor": sec_tensor, "coeff": sec_coeff, "norms": sec_norms}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(SECTIONS)):

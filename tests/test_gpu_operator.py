@@ -478,3 +478,89 @@ def test_csr_gs_abi_bitwise(cuda):
     rows = g["csr_rows"][:3]
     ok.csr_gs(rows, A.indptr, A.indices, A.data, A.diagonal(), want, g["csr_f"], 0.9)
     assert np.array_equal(got, want)
+
+
+# -- the FMA edge-flux path (fast=True: the bench's default arithmetic) ----
+# Contract (BASELINE north star): within 1e-12 relative of the reference
+# order, measured against max |A u| of the bitwise result.
+TOL_FAST = 1e-12
+
+
+def _fast_vs(exact, fast):
+    return np.abs(fast - exact).max() / np.abs(exact).max()
+
+
+def test_fast_config1_against_oracle(cuda):
+    grid = M.RefinedGrid(case_mesh("c1"), 4)
+    kf = sample_nodal(k_c1(), grid)
+    u = np.random.default_rng(0).uniform(-1, 1, grid.n_nodes)
+    want = CpuOperator(grid, "scaling", kf).apply(u)
+    op = Operator(grid, "scaling", kf, fast=True)
+    assert op._vol_flags() & 6 == 6            # the FMA mirror kernel
+    assert _fast_vs(want, op.apply(u)) <= TOL_FAST
+    f = np.random.default_rng(1).uniform(-1, 1, grid.n_nodes)
+    assert _fast_vs(CpuOperator(grid, "scaling", kf).residual(u, f),
+                    op.residual(u, f)) <= TOL_FAST
+
+
+@pytest.mark.slow
+def test_fast_config3_full_size(cuda):
+    """Config 3 at full size (48 elements, level 7): the FMA path against
+    the bitwise path (itself pinned by test_config3_full_size_checksums),
+    apply and residual."""
+    torch = cuda
+    grid = M.RefinedGrid(case_mesh("c3"), 7)
+    kf = sample_nodal(k_c3(), grid)
+    rng = np.random.default_rng(17)
+    u = torch.as_tensor(rng.uniform(-1, 1, grid.n_nodes), device="cuda")
+    f = torch.as_tensor(rng.uniform(-1, 1, grid.n_nodes), device="cuda")
+    exact, fast = Operator(grid, "scaling", kf), Operator(grid, "scaling", kf, fast=True)
+    a, b = exact.apply(u), fast.apply(u)
+    assert ((a - b).abs().max() / a.abs().max()).item() <= TOL_FAST
+    a, b = exact.residual(u, f), fast.residual(u, f)
+    assert ((a - b).abs().max() / a.abs().max()).item() <= TOL_FAST
+
+
+@pytest.mark.slow
+def test_fast_config5_elements(cuda):
+    """Config 5 (96 elements, level 8): three elements' volume rows of the
+    FMA path against the C oracle of the reference kernel."""
+    from tests.cases import k_c5
+    torch = cuda
+    grid = M.RefinedGrid(case_mesh("c5"), 8)
+    kf = sample_nodal(k_c5(), grid)
+    op = Operator(grid, "scaling", kf, fast=True)
+    u = np.random.default_rng(5).uniform(-1, 1, grid.n_nodes)
+    out = op.apply(torch.as_tensor(u, device="cuda"))
+    nvol = grid.nodes_per_volume
+    for t in (0, 47, 95):
+        want = ok.apply_scaling_3d(grid.n, grid.lat.base, u[grid.elem_gidx[t]], kf.values[t],
+                                   op._sh[t])
+        s0 = int(grid.vol_start[t])
+        assert _fast_vs(want, out[s0:s0 + nvol].cpu().numpy()) <= TOL_FAST, t
+
+
+@pytest.mark.parametrize("fast", [False, True])
+def test_config5_slab_whole_vector_against_oracle(cuda, fast):
+    """The config-5 mesh (96-element slab) at a reduced level, whole vector
+    against the CPU operator (reference algorithm, independent assembly of
+    the surface rows): volume rows bitwise (fast: 1e-12), surface rows
+    1e-13, Dirichlet rows exact — apply and residual."""
+    from tests.cases import k_c5
+    grid = M.RefinedGrid(case_mesh("c5"), 5)
+    kf = sample_nodal(k_c5(), grid)
+    rng = np.random.default_rng(55)
+    u = rng.uniform(-1, 1, grid.n_nodes)
+    f = rng.uniform(-1, 1, grid.n_nodes)
+    cpu = CpuOperator(grid, "scaling", kf)
+    op = Operator(grid, "scaling", kf, fast=fast)
+    vol = _vol_mask(grid)
+    for got, want in ((op.apply(u), cpu.apply(u)), (op.residual(u, f), cpu.residual(u, f))):
+        scale = np.abs(want).max()
+        if fast:
+            assert np.abs(got[vol] - want[vol]).max() <= TOL_FAST * scale
+        else:
+            assert np.array_equal(got[vol], want[vol])
+        assert np.abs(got[~vol] - want[~vol]).max() <= TOL_SURF * scale
+        d = grid.dirichlet_mask
+        assert np.array_equal(got[d], want[d])

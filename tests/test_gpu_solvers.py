@@ -11,7 +11,7 @@ from tests.conftest import golden
 from paper_1709_06793_b200 import mesh as M
 from paper_1709_06793_b200.coefficients import cos3d
 from paper_1709_06793_b200.multigrid import GridHierarchy, prolongation_matrix, solve, vcycle
-from tests.cases import case_mesh, c4_field, k_c2
+from tests.cases import c2_error_norms, case_mesh, c4_field, k_c2
 
 pytestmark = pytest.mark.gpu
 
@@ -94,11 +94,12 @@ def test_config2_cg_matches_reference(cuda, variant):
     assert res <= 1.5e-10 * g[f"{variant}_b"]
     assert abs(res - g[f"{variant}_res"]) <= 0.2 * g[f"{variant}_res"]
     assert np.abs(u[::97] - g[f"{variant}_u_sample"]).max() <= 1e-8 * np.abs(u).max()
-    X = grid.node_coords
-    exact = np.sin(np.pi * X[:, 0]) * np.sin(np.pi * X[:, 1]) * np.sin(np.pi * X[:, 2])
-    free = ~grid.dirichlet_mask
-    l2d = np.sqrt(grid.h_ref() ** 3 * np.sum((u - exact)[free] ** 2))
+    # discretisation errors against the reference's analysis.error_norms
+    # (restated in tests/cases.py, pinned by tests/test_norms_golden.py)
+    l2d, l2q, h1 = c2_error_norms(u, grid)
     assert abs(l2d - g[f"{variant}_l2d"]) <= 1e-6 * g[f"{variant}_l2d"]
+    assert abs(l2q - g[f"{variant}_l2"]) <= 1e-6 * g[f"{variant}_l2"]
+    assert abs(h1 - g[f"{variant}_h1"]) <= 1e-6 * g[f"{variant}_h1"]
 
 
 @pytest.mark.slow
