@@ -132,6 +132,23 @@ typedef struct hhg_grid {
   const int32_t *mtiles;   /* hhg_volume_tile_cols_mirror() columns wide     */
 } hhg_grid;
 
+/* one free macro face whose interior points are surface rows (face-tiled
+ * surface kernel): incident elements tet[0] < tet[1] (tet[1] = -1: the other
+ * side is on another rank), the face's boundary class in each, and the
+ * affine map from face-local (a, b), a, b >= 1, a + b <= n - 1, to element
+ * lattice coordinates: (i, j, k) = c[e] + (A[e][0] a + A[e][1] b,
+ * A[e][2] a + A[e][3] b, A[e][4] a + A[e][5] b) */
+typedef struct hhg_face {
+  int32_t tet[2];
+  int32_t cls[2];
+  int32_t A[2][6];
+  int32_t c[2][3];
+  int32_t nodal;           /* 1: nodal-integration rows (hybrid / nodal)     */
+  int32_t pad_;
+  int64_t fs;              /* global id of the face's first interior point   */
+  int64_t rbase;           /* surface-row index of fs (rows are sorted)      */
+} hhg_face;
+
 typedef struct hhg_surface {
   int64_t nrows;           /* non-Dirichlet surface rows                     */
   const int64_t *rows;     /* [nrows] global ids                             */
@@ -156,6 +173,16 @@ typedef struct hhg_surface {
   const uint8_t *p_nodal;  /* [ninc] row of this incidence is a nodal row    */
   const int32_t *row_inc;  /* [ninc] element-major index, row-major order    */
   double *partial;         /* [ninc] scratch                                 */
+  /* face-tiled apply (hhg_surface_apply_csr): the rows of nfaces free macro
+   * faces from face_tiles (face, a0, b0, 0) of 32 x 8 points, the remaining
+   * (edge / vertex) rows nsub row indices in sub_rows; nfaces = 0: every
+   * row through the precomputed rows                                     */
+  int64_t nfaces;
+  const hhg_face *faces;
+  int64_t nface_tiles;
+  const int32_t *face_tiles;
+  int64_t nsub;
+  const int32_t *sub_rows;
 } hhg_surface;
 
 /* refresh the ghost layers: ghost[e] = u[shell_gid[e]] */
@@ -189,6 +216,25 @@ int hhg_axpy_ratio(int64_t n, const double *num, const double *den,
 /* p = r + (num/den) p */
 int hhg_xpay_ratio(int64_t n, const double *num, const double *den,
                    const double *r, double *p, void *stream);
+
+/* fused CG / PCG updates (multigrid.py:169-194), scalars in device memory,
+ * one pass each with the next dot's partials formed on the way (work: >= 1024
+ * doubles; bitwise the separate axpy / dot sequence):
+ *   cg_update : a = rs/pAp; x += a p; r -= a Ap; rs_new = r.r (over the
+ *               entries with mask != 0 when mask is not NULL)
+ *   pcg_update: a = rz/pAp; x += a p; r_new = r - a Ap; rr_new = r_new.r_new
+ *   dot2      : result[0] = (a - b).c, result[1] = a.c (work >= 2048)
+ *   dot_masked: result[0] = sum over mask != 0 of x y (sharded vectors)    */
+int hhg_cg_update(int64_t n, const double *rs, const double *pAp, const double *p,
+                  const double *Ap, double *x, double *r, const uint8_t *mask,
+                  double *work, double *rs_new, void *stream);
+int hhg_pcg_update(int64_t n, const double *rz, const double *pAp, const double *p,
+                   const double *Ap, double *x, const double *r, double *r_new,
+                   double *work, double *rr_new, void *stream);
+int hhg_dot2(int64_t n, const double *a, const double *b, const double *c, double *work,
+             double *result, void *stream);
+int hhg_dot_masked(int64_t n, const double *x, const double *y, const uint8_t *mask,
+                   double *work, double *result, void *stream);
 
 /* y = A x for a CSR matrix (prolongation, restriction = P^T as a CSR of
  * the transpose); rows accumulate in stored column order (bitwise scipy) */

@@ -10,7 +10,8 @@ import ctypes
 import os
 from pathlib import Path
 
-__all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "HhgSurfaceGS", "check", "HhgError",
+__all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "HhgSurfaceGS", "HhgFace", "check",
+           "HhgError",
            "VAR", "FLAG_RESIDUAL", "FLAG_FAST", "FLAG_MIRROR", "EXPORTS"]
 
 LIB_PATH = Path(__file__).resolve().parent / "libhhg_b200.so"
@@ -42,7 +43,16 @@ class HhgSurface(ctypes.Structure):
                 ("inc_cls", vp), ("psh", vp), ("pfac", vp),
                 ("ndir", ctypes.c_int64), ("dir_ids", vp),
                 ("ninc", ctypes.c_int64), ("p_tet", vp), ("p_code", vp),
-                ("p_cls", vp), ("p_nodal", vp), ("row_inc", vp), ("partial", vp)]
+                ("p_cls", vp), ("p_nodal", vp), ("row_inc", vp), ("partial", vp),
+                ("nfaces", ctypes.c_int64), ("faces", vp), ("nface_tiles", ctypes.c_int64),
+                ("face_tiles", vp), ("nsub", ctypes.c_int64), ("sub_rows", vp)]
+
+
+class HhgFace(ctypes.Structure):
+    _fields_ = [("tet", ctypes.c_int32 * 2), ("cls", ctypes.c_int32 * 2),
+                ("A", (ctypes.c_int32 * 6) * 2), ("c", (ctypes.c_int32 * 3) * 2),
+                ("nodal", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("fs", ctypes.c_int64), ("rbase", ctypes.c_int64)]
 
 
 class HhgSurfaceGS(ctypes.Structure):
@@ -126,6 +136,12 @@ EXPORTS = {
     "hhg_axpy_ratio": (ctypes.c_int, [ctypes.c_int64, vp, vp, ctypes.c_double, vp,
                                       vp, vp]),
     "hhg_xpay_ratio": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),
+    "hhg_cg_update": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                     vp]),
+    "hhg_pcg_update": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                      vp]),
+    "hhg_dot2": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp]),
+    "hhg_dot_masked": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp]),
     "hhg_csr_spmv": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp,
                                     ctypes.c_int, vp]),
     "hhg_scatter_zero": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp]),

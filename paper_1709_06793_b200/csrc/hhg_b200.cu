@@ -17,6 +17,7 @@
 #include "hhg_common.cuh"
 #include "hhg_smooth.cuh"
 #include "hhg_surface.cuh"
+#include "hhg_surface_face.cuh"
 #include "hhg_tensor.cuh"
 #include "hhg_volume.cuh"
 #ifndef HHG_VOLUME_TMA
@@ -737,16 +738,34 @@ static int surface_csr(const hhg_grid *g, const hhg_surface *s, const hhg_surfac
   G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
   G.ent_col = gs->ent_col;
   G.ent_val = gs->ent_val;
+  G.shell_gid = reinterpret_cast<const long long *>(g->shell_gid);
 #ifndef HHG_FUSE_DIRICHLET
 #define HHG_FUSE_DIRICHLET 0
 #endif
   const long long *ids = reinterpret_cast<const long long *>(s->dir_ids);
   const long long nd = HHG_FUSE_DIRICHLET ? s->ndir : 0;
-  const long long total = s->nrows + nd;   // surface rows (then Dirichlet rows)
+  const bool faced = s->nfaces > 0 && s->nface_tiles > 0;
+  if (faced) {   // face rows tiled per macro face, edge / vertex rows below
+    const int4 *ft = reinterpret_cast<const int4 *>(s->face_tiles);
+    const int nb = (int)s->nface_tiles, nt = FACE_TA * FACE_TB;
+    const bool mixed = s->pfac != nullptr;
+    if (res) {
+      if (mixed) surface_face_kernel<true, true><<<nb, nt, 0, S(stream)>>>(G, s->faces, ft, out, push);
+      else surface_face_kernel<true, false><<<nb, nt, 0, S(stream)>>>(G, s->faces, ft, out, push);
+    } else {
+      if (mixed) surface_face_kernel<false, true><<<nb, nt, 0, S(stream)>>>(G, s->faces, ft, out, push);
+      else surface_face_kernel<false, false><<<nb, nt, 0, S(stream)>>>(G, s->faces, ft, out, push);
+    }
+    int rc = check("surface_face_kernel");
+    if (rc) return rc;
+  }
+  const int *sub = faced ? s->sub_rows : nullptr;
+  const long long nsub = faced ? s->nsub : 0;
+  const long long total = (faced ? nsub : s->nrows) + nd;   // rows (then Dirichlet rows)
   if (total > 0) {
     const int blocks = (int)((total + 127) / 128);
-    if (res) surface_csr_kernel<true><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids);
-    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids, push);
+    if (res) surface_csr_kernel<true><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids, SurfPush{}, sub, nsub);
+    else surface_csr_kernel<false><<<blocks, 128, 0, S(stream)>>>(G, out, nd, ids, push, sub, nsub);
     int rc = check("surface_csr_kernel");
     if (rc) return rc;
   }

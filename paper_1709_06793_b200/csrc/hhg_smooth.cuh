@@ -367,18 +367,23 @@ struct SurfPush {
 
 template <bool RES>
 __global__ void surface_csr_kernel(SurfGSDesc G, double *out, long long ndir,
-                                   const long long *dir_ids, SurfPush push = SurfPush{}) {
-  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+                                   const long long *dir_ids, SurfPush push = SurfPush{},
+                                   const int *sub = nullptr, long long nsub = 0) {
+  const long long x0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const SurfDesc &D = G.s;
-  if (r >= D.nrows) {
-    // Dirichlet rows ride along in the same launch: identity (0 for f - Au)
-    const long long e = r - D.nrows;
+  // rows: all of them, or the sub-list (edge / vertex rows next to the
+  // face-tiled kernel); Dirichlet rows ride along after them
+  const long long nr = sub ? nsub : D.nrows;
+  if (x0 >= nr) {
+    // Dirichlet rows: identity (0 for f - Au)
+    const long long e = x0 - nr;
     if (e < ndir) {
       const long long g = dir_ids[e];
       out[g] = RES ? 0.0 : D.u[g];
     }
     return;
   }
+  const long long r = sub ? (long long)sub[x0] : x0;
   const long long gid = D.rows[r];
   const double v0 = D.u[gid];
   long long e = G.ent_ptr[r];

@@ -44,6 +44,100 @@ __global__ void dot_final(int nb, const double *work, double *result) {
   if (threadIdx.x == 0) result[0] = acc;
 }
 
+// ---------------------------------------------------------------------------
+// fused CG / PCG updates (multigrid.py:169-194): one pass per update with
+// the next dot product's partials formed on the way.  Launched with the dot
+// geometry (dot_blocks x 256, grid-stride), so every partial sum is formed
+// in exactly the order dot_partial would form it: the iterates are bitwise
+// those of the separate axpy / dot sequence.
+// ---------------------------------------------------------------------------
+
+// a = rs / pAp;  x += a p;  r -= a Ap;  work[block] = partial sum of r.r
+// (over the entries with mask != 0 when a mask is given: sharded vectors)
+__global__ void cg_update_kernel(long long n, const double *rs, const double *pAp,
+                                 const double *__restrict__ p, const double *__restrict__ Ap,
+                                 double *__restrict__ x, double *__restrict__ r,
+                                 const unsigned char *__restrict__ mask, double *work) {
+  __shared__ double sh[32];
+  const double a = 1.0 * (rs[0] / pAp[0]);
+  const double na = -1.0 * (rs[0] / pAp[0]);
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] += a * p[i];
+    const double ri = r[i] + na * Ap[i];
+    r[i] = ri;
+    if (!mask || mask[i]) acc = fma(ri, ri, acc);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) work[blockIdx.x] = acc;
+}
+
+// PCG: a = rz / pAp;  x += a p;  rn = r - a Ap;  work = partials of rn.rn
+__global__ void pcg_update_kernel(long long n, const double *rz, const double *pAp,
+                                  const double *__restrict__ p, const double *__restrict__ Ap,
+                                  double *__restrict__ x, const double *__restrict__ r,
+                                  double *__restrict__ rn, double *work) {
+  __shared__ double sh[32];
+  const double a = rz[0] / pAp[0];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    x[i] += a * p[i];
+    const double v = r[i] - a * Ap[i];
+    rn[i] = v;
+    acc = fma(v, v, acc);
+  }
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) work[blockIdx.x] = acc;
+}
+
+// two dots in one pass: work[b] = partial of (a - b).c, work[nb + b] = a.c
+__global__ void dot2_partial(long long n, const double *__restrict__ a,
+                             const double *__restrict__ b, const double *__restrict__ c,
+                             double *work) {
+  __shared__ double sh[32];
+  double d1 = 0.0, d2 = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double ci = c[i], ai = a[i];
+    d1 = fma(ai - b[i], ci, d1);
+    d2 = fma(ai, ci, d2);
+  }
+  d1 = block_sum(d1, sh);
+  __syncthreads();
+  d2 = block_sum(d2, sh);
+  if (threadIdx.x == 0) {
+    work[blockIdx.x] = d1;
+    work[gridDim.x + blockIdx.x] = d2;
+  }
+}
+
+// owner-masked dot (sharded vectors: every shared node counted once)
+__global__ void dot_masked_partial(long long n, const double *__restrict__ x,
+                                   const double *__restrict__ y,
+                                   const unsigned char *__restrict__ mask, double *work) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    if (mask[i]) acc = fma(x[i], y[i], acc);
+  acc = block_sum(acc, sh);
+  if (threadIdx.x == 0) work[blockIdx.x] = acc;
+}
+
+// final sums of k partial arrays of nb entries each: result[q] = sum work[q nb ..]
+__global__ void dot_final_multi(int nb, int k, const double *work, double *result) {
+  __shared__ double sh[32];
+  for (int q = 0; q < k; ++q) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) acc += work[q * nb + i];
+    acc = block_sum(acc, sh);
+    if (threadIdx.x == 0) result[q] = acc;
+    __syncthreads();
+  }
+}
+
 __global__ void axpy_ratio_kernel(long long n, const double *num, const double *den,
                                   double sign, const double *__restrict__ x,
                                   double *__restrict__ y) {
@@ -98,6 +192,58 @@ int hhg_dot(int64_t n, const double *x, const double *y, double *work, double *r
   g_launches.fetch_add(1, std::memory_order_relaxed);
   hhg::dot_final<<<1, 1024, 0, st>>>(nb, work, result);
   return check("dot");
+}
+
+static inline int dot_blocks(long long n) {
+  int nb = (int)((n + 255) / 256);
+  if (nb > hhg::DOT_BLOCKS) nb = hhg::DOT_BLOCKS;
+  return nb < 1 ? 1 : nb;
+}
+
+int hhg_cg_update(int64_t n, const double *rs, const double *pAp, const double *p,
+                  const double *Ap, double *x, double *r, const uint8_t *mask, double *work,
+                  double *rs_new, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = dot_blocks(n);
+  hhg::cg_update_kernel<<<nb, 256, 0, st>>>(n, rs, pAp, p, Ap, x, r, mask, work);
+  int rc = check("cg_update_kernel");
+  if (rc) return rc;
+  hhg::dot_final<<<1, 1024, 0, st>>>(nb, work, rs_new);
+  return check("dot_final");
+}
+
+int hhg_pcg_update(int64_t n, const double *rz, const double *pAp, const double *p,
+                   const double *Ap, double *x, const double *r, double *r_new, double *work,
+                   double *rr_new, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = dot_blocks(n);
+  hhg::pcg_update_kernel<<<nb, 256, 0, st>>>(n, rz, pAp, p, Ap, x, r, r_new, work);
+  int rc = check("pcg_update_kernel");
+  if (rc) return rc;
+  hhg::dot_final<<<1, 1024, 0, st>>>(nb, work, rr_new);
+  return check("dot_final");
+}
+
+int hhg_dot2(int64_t n, const double *a, const double *b, const double *c, double *work,
+             double *result, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = dot_blocks(n);
+  hhg::dot2_partial<<<nb, 256, 0, st>>>(n, a, b, c, work);
+  int rc = check("dot2_partial");
+  if (rc) return rc;
+  hhg::dot_final_multi<<<1, 1024, 0, st>>>(nb, 2, work, result);
+  return check("dot_final_multi");
+}
+
+int hhg_dot_masked(int64_t n, const double *x, const double *y, const uint8_t *mask,
+                   double *work, double *result, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int nb = dot_blocks(n);
+  hhg::dot_masked_partial<<<nb, 256, 0, st>>>(n, x, y, mask, work);
+  int rc = check("dot_masked_partial");
+  if (rc) return rc;
+  hhg::dot_final<<<1, 1024, 0, st>>>(nb, work, result);
+  return check("dot_final");
 }
 
 int hhg_axpy_ratio(int64_t n, const double *num, const double *den, double sign,

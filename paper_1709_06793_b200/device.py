@@ -29,7 +29,7 @@ from .mesh import SimplexLattice, lattice_size
 from .reference_stencils import CLASS_OF_MASK, class_element_masks
 from .mesh import DIRS_3D
 
-__all__ = ["shell_layout", "volume_tiles", "GridTables", "SurfaceTables",
+__all__ = ["shell_layout", "volume_tiles", "GridTables", "SurfaceTables", "FaceTables",
            "DeviceGrid", "DeviceSurface", "require_cuda"]
 
 
@@ -218,6 +218,104 @@ class SurfaceTables:
         return np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
 
 
+FACE_TA, FACE_TB = 32, 8     # face tile of surface_face_kernel (hhg_surface_face.cuh)
+
+# (i, j, k) = c + A (a, b) on the face opposite local vertex f (barycentric
+# slot f = 0 is n - i - j - k, slots 1..3 are i, j, k), a along the fastest
+# lattice direction available on that face
+_FACE_PATTERN = {3: ((1, 0, 0, 1, 0, 0), (0, 0, 0)),     # k = 0: (a, b, 0)
+                 2: ((1, 0, 0, 0, 0, 1), (0, 0, 0)),     # j = 0: (a, 0, b)
+                 1: ((0, 0, 1, 0, 0, 1), (0, 0, 0)),     # i = 0: (0, a, b)
+                 0: ((1, 0, 0, 1, -1, -1), None)}        # i+j+k = n: (a, b, n-a-b)
+
+
+class FaceTables:
+    """Free macro faces for the face-tiled surface kernel: per face its
+    incident elements in ascending order, the boundary class of the face in
+    each, the affine maps face-local (a, b) -> element lattice (i, j, k), the
+    global id / row index of its first interior point; the 32 x 8 tiles; and
+    the remaining surface rows (macro edges and vertices) as a sub-list."""
+
+    def __init__(self, grid, gt: GridTables, st: SurfaceTables):
+        n = grid.n
+        m = grid.macro
+        rows = np.asarray(st.rows)
+        npf = grid.nodes_per_face
+        recs, tiles = [], []
+        covered = np.zeros(len(rows), dtype=bool)
+        inc = [[] for _ in range(len(m.faces))]
+        if n >= 4:
+            for t in range(m.n_elements):
+                for f in range(4):
+                    inc[int(m.elem_faces[t, f])].append((t, f))
+        lat = grid.lat
+        for F, tf in enumerate(inc):
+            if not tf or len(tf) > 2:
+                continue
+            fs = int(grid.face_start[F])
+            r0 = int(np.searchsorted(rows, fs))
+            if r0 + npf > len(rows) or rows[r0] != fs or rows[r0 + npf - 1] != fs + npf - 1:
+                continue                      # Dirichlet face (no rows) or not a plain block
+            tf = sorted(tf)
+            A, c, cls = [], [], []
+            t1, f1 = tf[0]
+            a1, c1 = _FACE_PATTERN[f1]
+            c1 = c1 if c1 is not None else (0, 0, n)
+            for e, (t, f) in enumerate(tf):
+                cls.append(CLASS_OF_MASK[1 << f])
+                if e == 0:
+                    A.append(a1)
+                    c.append(c1)
+                    continue
+                pts = []
+                for (pa, pb) in ((1, 1), (2, 1), (1, 2), (n - 2, 1), (1, n - 2)):
+                    i = c1[0] + a1[0] * pa + a1[1] * pb
+                    j = c1[1] + a1[2] * pa + a1[3] * pb
+                    k = c1[2] + a1[4] * pa + a1[5] * pb
+                    gid = grid.elem_gidx[t1, lat.base[k, j] + i]
+                    pos = np.nonzero(gt.shell_gid[t] == gid)[0]
+                    if len(pos) != 1:
+                        raise AssertionError("face point not on the neighbour's shell")
+                    pts.append(lat.coords[gt.shell_pos[pos[0]]].astype(np.int64))
+                p11, p21, p12 = pts[:3]
+                da, db = p21 - p11, p12 - p11
+                cc = p11 - da - db
+                for (pa, pb), p in zip(((n - 2, 1), (1, n - 2)), pts[3:]):
+                    if not np.array_equal(cc + da * pa + db * pb, p):
+                        raise AssertionError("face map is not affine")
+                A.append((int(da[0]), int(db[0]), int(da[1]), int(db[1]), int(da[2]),
+                          int(db[2])))
+                c.append(tuple(int(x) for x in cc))
+            recs.append((tuple(x for x, _ in tf) + ((-1,) if len(tf) == 1 else ()),
+                         tuple(cls) + ((0,) if len(tf) == 1 else ()),
+                         tuple(A) + (((0,) * 6,) if len(tf) == 1 else ()),
+                         tuple(c) + (((0, 0, 0),) if len(tf) == 1 else ()),
+                         int(st.row_nodal[r0]), fs, r0))
+            covered[r0:r0 + npf] = True
+            fid = len(recs) - 1
+            for b0 in range(1, n - 1, FACE_TB):
+                for a0 in range(1, n - b0, FACE_TA):
+                    tiles.append((fid, a0, b0, 0))
+        self.faces = recs
+        self.tiles = np.ascontiguousarray(np.array(tiles, dtype=np.int32).reshape(-1, 4))
+        self.sub_rows = np.ascontiguousarray(np.nonzero(~covered)[0].astype(np.int32))
+
+    def packed(self):
+        """The faces as an array of hhg_face structs (bytes)."""
+        from ._lib import HhgFace
+        arr = (HhgFace * max(len(self.faces), 1))()
+        for x, (tet, cls, A, c, nodal, fs, rb) in enumerate(self.faces):
+            h = arr[x]
+            for e in range(2):
+                h.tet[e], h.cls[e] = tet[e], cls[e]
+                for q in range(6):
+                    h.A[e][q] = A[e][q]
+                for q in range(3):
+                    h.c[e][q] = c[e][q]
+            h.nodal, h.fs, h.rbase = nodal, fs, rb
+        return np.frombuffer(bytes(arr), dtype=np.uint8).copy()
+
+
 class DeviceGrid:
     """Torch buffers + the hhg_grid descriptor of one level."""
 
@@ -255,7 +353,7 @@ class DeviceGrid:
 
 
 class DeviceSurface:
-    def __init__(self, st: SurfaceTables, psh, pfac, tensor=None):
+    def __init__(self, st: SurfaceTables, psh, pfac, tensor=None, faces: FaceTables = None):
         torch = require_cuda()
         dev = torch.device("cuda")
         t = lambda a: torch.as_tensor(np.ascontiguousarray(a), device=dev)
@@ -294,6 +392,18 @@ class DeviceSurface:
         d.p_nodal = self.p_nodal.data_ptr()
         d.row_inc = self.row_inc.data_ptr()
         d.partial = self.partial.data_ptr()
+        d.nfaces = 0
+        self.faces = faces
+        if faces is not None and len(faces.faces) and tensor is None:
+            self.face_buf = t(faces.packed())
+            self.face_tiles = t(faces.tiles)
+            self.sub_rows = t(faces.sub_rows if len(faces.sub_rows) else np.zeros(1, np.int32))
+            d.nfaces = len(faces.faces)
+            d.faces = self.face_buf.data_ptr()
+            d.nface_tiles = len(faces.tiles)
+            d.face_tiles = self.face_tiles.data_ptr()
+            d.nsub = len(faces.sub_rows)
+            d.sub_rows = self.sub_rows.data_ptr()
         self.desc = d
         self.ref = ctypes.byref(d)
         self._levels = None

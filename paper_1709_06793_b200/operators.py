@@ -25,7 +25,7 @@ from . import _lib
 from ._lib import check, lib
 from .coefficients import CoefficientField, TensorCoefficient
 from .costmodel import analytic_count
-from .device import (DeviceGrid, DeviceSurface, GridTables, SurfaceTables,
+from .device import (DeviceGrid, DeviceSurface, FaceTables, GridTables, SurfaceTables,
                      require_cuda)
 from .mesh import PrimitiveKind
 from .reference_stencils import (classify_edge_types, environment,
@@ -77,8 +77,8 @@ class Operator:
         self.ma2_marked = None
         self._stored = None
         self.fast = bool(fast)
-        if surface_mode not in ("csr", "matrix-free"):
-            raise ValueError("surface_mode must be 'csr' or 'matrix-free'")
+        if surface_mode not in ("csr", "face", "matrix-free"):
+            raise ValueError("surface_mode must be 'csr', 'face' or 'matrix-free'")
         self.surface_mode = surface_mode
         if variant == "const":
             self.const_value = 1.0 if coeff is None else float(coeff)
@@ -90,7 +90,7 @@ class Operator:
                                  "coefficients only")
             if coeff.grid is not grid:
                 raise ValueError("coefficient sampled on a different grid")
-            if surface_mode != "csr":
+            if surface_mode not in ("csr", "face"):
                 raise ValueError("tensor operators use the precomputed surface rows")
         else:
             if not isinstance(coeff, CoefficientField) and not (
@@ -211,8 +211,11 @@ class Operator:
                 kc = self.coeff.values
             dg = DeviceGrid(gt, kc)
             st = SurfaceTables(grid, gt, self._nodal_kinds)
+            faces = FaceTables(grid, gt, st) if (self.surface_mode == "face" and
+                                                 not self.is_tensor) else None
             ds = DeviceSurface(st, self._psh, self._pfac,
-                               tensor=(self.coeff.M, km) if self.is_tensor else None)
+                               tensor=(self.coeff.M, km) if self.is_tensor else None,
+                               faces=faces)
             coef = torch.as_tensor(self._coef, device="cuda").reshape(-1)
             w = None
             if self._stored is not None:
@@ -314,7 +317,7 @@ class Operator:
         flags = self._vol_flags(residual=f is not None)
         res = flags & _lib.FLAG_RESIDUAL
         fp = f.data_ptr() if f is not None else None
-        concurrent = self.surface_mode == "csr" and after_surface is not None
+        concurrent = self.surface_mode != "matrix-free" and after_surface is not None
         # the surface rows read shell values from the ghost layer: refresh first
         check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
         if concurrent:
@@ -357,7 +360,7 @@ class Operator:
         (setup on first use, `surface_mode="csr"`), else matrix-free.
         ``push`` = (slot_ptr, dst0, dst1, split): also store the interface
         rows into the neighbours' receive buffers (shard.PeerExchange)."""
-        if self.surface_mode == "csr":
+        if self.surface_mode != "matrix-free":
             c = ds.csr(dg)
             if push is not None and not res_flag:
                 check(lib.hhg_surface_apply_csr_push(dg.ref, ds.ref, c["ref"], du.data_ptr(),
@@ -460,7 +463,7 @@ class Operator:
         chunks = self._chunks()
         flags = self._vol_flags(residual=res)
         wp = D["w"].data_ptr() if D["w"] is not None else None
-        if self.surface_mode == "csr":
+        if self.surface_mode != "matrix-free":
             ds.csr(dg)          # one-time fill on this stream, before the others join it
         cur = torch.cuda.current_stream()
         for st in P["streams"]:

@@ -129,9 +129,10 @@ class PeerExchange:
 
     def __init__(self, op, imap: InterfaceMap):
         import torch
-        if getattr(op, "surface_mode", "csr") != "csr":
-            # the pushes are stored by the precomputed-row surface kernel only
-            raise ValueError("peer exchange needs surface_mode='csr'")
+        if getattr(op, "surface_mode", "csr") == "matrix-free":
+            # the pushes are stored by the precomputed-row / face-tiled
+            # surface kernels only
+            raise ValueError("peer exchange needs surface_mode 'csr' or 'face'")
         self.torch, self.op, self.imap = torch, op, imap
         self.rank = imap.rank
         D = op._device()
@@ -335,23 +336,49 @@ class ShardedOperator:
         """f - A u, zero on Dirichlet rows."""
         return (f - self.apply(u)) * self._mask("free", u.device)
 
-    def dot(self, a, b):
+    def dot(self, a, b, out=None):
         """Global dot: every shared node counted once (owner = lower rank),
-        Dirichlet entries excluded, one all-reduce."""
+        Dirichlet entries excluded, one all-reduce of one double.  On the
+        device: the owner-masked dot kernel into a device scalar (``out``,
+        kept on the device: no host round trip)."""
+        if a.is_cuda:
+            from .multigrid import DeviceVec
+            if getattr(self, "_vec", None) is None:
+                self._vec = DeviceVec(self.torch)
+            m = self._mask_u8(a.device)
+            if out is None:
+                out = self.torch.zeros(1, dtype=self.torch.float64, device=a.device)
+            self._vec.dot_masked(a, b, m, out)
+            self.dist.all_reduce(out)
+            return out
         local = (a * b * self._mask("owned", a.device)).sum().reshape(1)
         self.dist.all_reduce(local)
         return local
+
+    def _mask_u8(self, device):
+        key = ("owned_u8", str(device))
+        if key not in self._masks:
+            self._masks[key] = self.torch.as_tensor(self._owned.astype(np.uint8), device=device)
+        return self._masks[key]
 
 
 def sharded_cg(sop: ShardedOperator, f, tol=1e-10, max_iter=10000):
     """Plain CG on the partitioned system (the reference's _cg,
     multigrid.py:169-194, with global dots): stop when ||r|| <= tol ||b||.
-    Returns (x, iterations, final residual norm)."""
+    Returns (x, iterations, final residual norm).
+
+    Device vectors: every update is a fused kernel with its scalars in
+    device memory (hhg_cg_update: x += a p, r -= a Ap and the owned partial
+    of r.r; hhg_xpay_ratio), dots are owner-masked with one all-reduce of a
+    device scalar, and the only host read per iteration is the stopping
+    test.  CPU vectors (gloo tests): the same sequence in torch."""
     torch = sop.torch
     free = sop._mask("free", f.device)
     x = torch.zeros_like(f)
     r = f * free
     p = r.clone()
+    if f.is_cuda:
+        return _sharded_cg_device(sop, x, r, p, tol, max_iter)
     rs = sop.dot(r, r)
     b0 = float(torch.sqrt(rs).item())
     sop.check()
@@ -370,4 +397,36 @@ def sharded_cg(sop: ShardedOperator, f, tol=1e-10, max_iter=10000):
             break
         p = r + (rs_new / rs) * p
         rs = rs_new
+    return x, it, res
+
+
+def _sharded_cg_device(sop, x, r, p, tol, max_iter):
+    torch = sop.torch
+    from .multigrid import DeviceVec
+    V = DeviceVec(torch)
+    sc = torch.zeros(4, dtype=torch.float64, device=x.device)
+    rs, pAp, rs_new = sc[0:1], sc[1:2], sc[2:3]
+    host = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+    sop.dot(r, r, out=rs)
+    b0 = float(np.sqrt(rs.item()))
+    sop.check()
+    if b0 == 0.0:
+        return x, 0, 0.0
+    owned = sop._mask_u8(x.device)
+    it, res = 0, b0
+    for it in range(1, max_iter + 1):
+        # p's Dirichlet entries stay 0 (r starts 0 there and every update
+        # keeps it), so the identity Dirichlet rows of A p are 0 as well
+        Ap = sop.apply(p)
+        sop.dot(p, Ap, out=pAp)
+        V.cg_update(rs, pAp, p, Ap, x, r, rs_new, owned)   # owned partial of r.r
+        sop.dist.all_reduce(rs_new)
+        host.copy_(rs_new, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        res = float(np.sqrt(host.item()))
+        sop.check()                       # host sync point: lost peer signals raise
+        if res <= tol * b0:
+            break
+        V.xpay(rs_new, rs, r, p)
+        rs.copy_(rs_new)
     return x, it, res

@@ -273,21 +273,29 @@ def test_large_grid_algebraic_properties(cuda):
     assert abs(s1 - s2) <= 1e-10 * abs(s1)
 
 
-@pytest.mark.parametrize("name", ["scaling", "nodal", "hybrid:wv+we"])
-def test_surface_modes_agree_bitwise(cuda, name):
-    """Precomputed surface rows (default) and the matrix-free surface kernels
+@pytest.mark.parametrize("name", ["scaling", "nodal", "hybrid:wv+we", "hybrid:wf"])
+@pytest.mark.parametrize("cfg", ["c3", "c5"])
+def test_surface_modes_agree_bitwise(cuda, name, cfg):
+    """The three executions of the surface rows - precomputed rows for every
+    row (default), face-tiled (face rows per macro face, edge / vertex rows
+    from the precomputed rows) and the matrix-free two-pass kernels -
     perform the same IEEE operations in the same order."""
-    grid = M.RefinedGrid(case_mesh("c3"), 4)
+    grid = M.RefinedGrid(case_mesh(cfg), 4)
     kf = sample_nodal(k_c3(), grid)
     hn, v = frozenset(), name
     if name.startswith("hybrid:"):
         hn, v = parse_hybrid_set(name.split(":", 1)[1]), "hybrid"
     u = np.random.default_rng(9).uniform(-1, 1, grid.n_nodes)
     f = np.random.default_rng(10).uniform(-1, 1, grid.n_nodes)
-    a = Operator(grid, v, kf, hybrid_nodal=hn)
+    a = Operator(grid, v, kf, hybrid_nodal=hn, surface_mode="face")
+    ds = a._device()["surf"]
+    assert ds.desc.nfaces > 0 and ds.desc.nsub < len(ds.st.rows)
     b = Operator(grid, v, kf, hybrid_nodal=hn, surface_mode="matrix-free")
-    assert np.array_equal(a.apply(u), b.apply(u))
-    assert np.array_equal(a.residual(u, f), b.residual(u, f))
+    c = Operator(grid, v, kf, hybrid_nodal=hn)         # every row from the precomputed rows
+    assert c._device()["surf"].desc.nfaces == 0
+    for x in (b, c):
+        assert np.array_equal(a.apply(u), x.apply(u))
+        assert np.array_equal(a.residual(u, f), x.residual(u, f))
 
 
 def test_surface_first_side_stream_path(cuda):
@@ -564,3 +572,37 @@ def test_config5_slab_whole_vector_against_oracle(cuda, fast):
         assert np.abs(got[~vol] - want[~vol]).max() <= TOL_SURF * scale
         d = grid.dirichlet_mask
         assert np.array_equal(got[d], want[d])
+
+
+@pytest.mark.parametrize("cfg,variant,kw", [("c3", "scaling", {}), ("c3", "scaling", {"fast": True}),
+                                            ("c5", "scaling", {"surface_mode": "face"}),
+                                            ("c3", "nodal", {}),
+                                            ("c3", "scaling", {"surface_mode": "matrix-free"})])
+def test_no_writes_outside_the_output(cuda, cfg, variant, kw):
+    """Canary check in place of compute-sanitizer (closed on this GPU pool):
+    the output vector is a view into a larger buffer whose guard bands hold
+    NaN sentinels; apply, residual and a smoothing sweep must leave them
+    untouched (and write every row: no NaN inside)."""
+    torch = cuda
+    grid = M.RefinedGrid(case_mesh(cfg), 4)
+    kf = sample_nodal(k_c3(), grid)
+    op = Operator(grid, variant, kf, **kw)
+    n, pad = grid.n_nodes, 4096
+    rng = np.random.default_rng(12)
+    u = torch.as_tensor(rng.uniform(-1, 1, n), device="cuda")
+    f = torch.as_tensor(rng.uniform(-1, 1, n), device="cuda")
+    buf = torch.full((n + 2 * pad,), float("nan"), dtype=torch.float64, device="cuda")
+    out = buf[pad:pad + n]
+    for call in (lambda: op.apply_device(u, out=out), lambda: op.apply_device(u, out=out, f=f)):
+        out.fill_(float("nan"))
+        call()
+        torch.cuda.synchronize()
+        assert torch.isnan(buf[:pad]).all() and torch.isnan(buf[pad + n:]).all()
+        assert not torch.isnan(out).any()
+    ubuf = torch.full((n + 2 * pad,), float("nan"), dtype=torch.float64, device="cuda")
+    uu = ubuf[pad:pad + n]
+    uu.copy_(u)
+    op.smooth_device(uu, f, sweeps=1)
+    torch.cuda.synchronize()
+    assert torch.isnan(ubuf[:pad]).all() and torch.isnan(ubuf[pad + n:]).all()
+    assert not torch.isnan(uu).any()

@@ -92,7 +92,11 @@ def test_config2_cg_matches_reference(cuda, variant):
     r[grid.dirichlet_mask] = 0.0
     res = np.linalg.norm(r[grid.interior_ids])
     assert res <= 1.5e-10 * g[f"{variant}_b"]
-    assert abs(res - g[f"{variant}_res"]) <= 0.2 * g[f"{variant}_res"]
+    # final true residual: the iterates differ from the reference's only by
+    # the summation order of surface rows / dots (1e-13 per apply); after
+    # 292 iterations the measured final residuals agree to 0.13%
+    # (tools/c2_probe.py: ratios 1.0013 scaling, 0.9992 nodal)
+    assert abs(res - g[f"{variant}_res"]) <= 0.01 * g[f"{variant}_res"]
     assert np.abs(u[::97] - g[f"{variant}_u_sample"]).max() <= 1e-8 * np.abs(u).max()
     # discretisation errors against the reference's analysis.error_norms
     # (restated in tests/cases.py, pinned by tests/test_norms_golden.py)
@@ -154,3 +158,35 @@ def test_vcycle_fixed_point(cuda, variant):
     u = ustar.copy()
     vcycle(hier, u, f, pre=2, post=2)
     assert np.abs(u - ustar).max() <= 1e-12 * np.abs(ustar).max()
+
+
+def test_sharded_cg_device_path_world1(cuda):
+    """sharded_cg on CUDA vectors (fused update kernel, owner-masked device
+    dots, all-reduce of device scalars) on a world-1 group: the same
+    iterates as the single-domain device CG, hence the same iteration
+    count and solution."""
+    import socket
+    import torch.distributed as dist
+    from paper_1709_06793_b200.shard import InterfaceMap, ShardedOperator, sharded_cg
+    torch = cuda
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=0,
+                            world_size=1)
+    try:
+        lvl = 4
+        hier = GridHierarchy(M.unit_cube_6(), lvl, "scaling", k_c2(), lmin=lvl, coarse_tol=1e-10)
+        grid = hier.grids[lvl]
+        op = hier.ops[lvl]
+        f = np.random.default_rng(3).normal(size=grid.n_nodes)
+        f[grid.dirichlet_mask] = 0.0
+        fd = torch.as_tensor(f, device="cuda")
+        rep = {}
+        want = hier._cg_device(op, fd, report=rep, graphs=False)
+        sop = ShardedOperator(op, InterfaceMap(grid, 0, 1, 1.0), dist, grid.dirichlet_mask)
+        x, its, res = sharded_cg(sop, fd, tol=1e-10)
+        assert its == rep["iterations"]
+        assert torch.equal(x, want)
+    finally:
+        dist.destroy_process_group()

@@ -1,5 +1,5 @@
 """Time the surface + Dirichlet rows of one apply on the config-5 workload:
-precomputed rows (default) vs the matrix-free two-pass kernels."""
+face-tiled (default), precomputed rows for every row, matrix-free two-pass."""
 import sys
 import time
 from pathlib import Path
@@ -17,10 +17,10 @@ level = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 grid = RefinedGrid(slab_mesh(0, 1), level)
 kf = sample_nodal(k_c5(), grid)
 u = torch.as_tensor(np.random.default_rng(0).uniform(-1, 1, grid.n_nodes), device="cuda")
-for mode in ("csr", "matrix-free"):
-    op = Operator(grid, "scaling", kf, surface_mode=mode)
-    out = op.apply_device(u)
+for mode in ("face-tiled", "csr", "matrix-free"):
+    op = Operator(grid, "scaling", kf, surface_mode="face" if mode == "face-tiled" else mode)
     D = op._device()
+    out = op.apply_device(u)
     st = torch.cuda.current_stream().cuda_stream
     for _ in range(3):
         op._surface(D["grid"], D["surf"], 0, u, None, out, st)
