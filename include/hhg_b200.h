@@ -137,14 +137,20 @@ typedef struct hhg_grid {
  * side is on another rank), the face's boundary class in each, and the
  * affine map from face-local (a, b), a, b >= 1, a + b <= n - 1, to element
  * lattice coordinates: (i, j, k) = c[e] + (A[e][0] a + A[e][1] b,
- * A[e][2] a + A[e][3] b, A[e][4] a + A[e][5] b) */
+ * A[e][2] a + A[e][3] b, A[e][4] a + A[e][5] b).  The element's layer next
+ * to the face is (i, j, k) = c[e] + nb[e] + A[e] (a, b); stencil direction d
+ * of a face point (a, b) reaches layer dl[e][d] (0 face, 1 inner, -1 none)
+ * at (a + da[e][d], b + db[e][d]). */
 typedef struct hhg_face {
   int32_t tet[2];
   int32_t cls[2];
   int32_t A[2][6];
   int32_t c[2][3];
+  int32_t nb[2][3];
+  int8_t dl[2][14];
+  int8_t da[2][14];
+  int8_t db[2][14];
   int32_t nodal;           /* 1: nodal-integration rows (hybrid / nodal)     */
-  int32_t pad_;
   int64_t fs;              /* global id of the face's first interior point   */
   int64_t rbase;           /* surface-row index of fs (rows are sorted)      */
 } hhg_face;
@@ -183,6 +189,15 @@ typedef struct hhg_surface {
   const int32_t *face_tiles;
   int64_t nsub;
   const int32_t *sub_rows;
+  /* static per-face layers of the face-tiled kernel: for face x, layer l
+   * (0 = the face, 1 + e = element e's layer next to it) and face-local
+   * (a, b), a, b in [-1, n+1]: the coefficient and the global id of that
+   * lattice point at [(x * 3 + l) * sq * sq + (b + 1) * sq + (a + 1)],
+   * sq = n + 3 (k = 0 / id = 0 outside the element)                      */
+  const double *face_k;
+  const int32_t *face_g;
+  int32_t face_sq;
+  int32_t pad_;
 } hhg_surface;
 
 /* refresh the ghost layers: ghost[e] = u[shell_gid[e]] */

@@ -45,13 +45,18 @@ class HhgSurface(ctypes.Structure):
                 ("ninc", ctypes.c_int64), ("p_tet", vp), ("p_code", vp),
                 ("p_cls", vp), ("p_nodal", vp), ("row_inc", vp), ("partial", vp),
                 ("nfaces", ctypes.c_int64), ("faces", vp), ("nface_tiles", ctypes.c_int64),
-                ("face_tiles", vp), ("nsub", ctypes.c_int64), ("sub_rows", vp)]
+                ("face_tiles", vp), ("nsub", ctypes.c_int64), ("sub_rows", vp),
+                ("face_k", vp), ("face_g", vp), ("face_sq", ctypes.c_int32),
+                ("pad_", ctypes.c_int32)]
 
 
 class HhgFace(ctypes.Structure):
     _fields_ = [("tet", ctypes.c_int32 * 2), ("cls", ctypes.c_int32 * 2),
                 ("A", (ctypes.c_int32 * 6) * 2), ("c", (ctypes.c_int32 * 3) * 2),
-                ("nodal", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("nb", (ctypes.c_int32 * 3) * 2),
+                ("dl", (ctypes.c_int8 * 14) * 2), ("da", (ctypes.c_int8 * 14) * 2),
+                ("db", (ctypes.c_int8 * 14) * 2),
+                ("nodal", ctypes.c_int32),
                 ("fs", ctypes.c_int64), ("rbase", ctypes.c_int64)]
 
 

@@ -746,15 +746,15 @@ static int surface_csr(const hhg_grid *g, const hhg_surface *s, const hhg_surfac
   const long long nd = HHG_FUSE_DIRICHLET ? s->ndir : 0;
   const bool faced = s->nfaces > 0 && s->nface_tiles > 0;
   if (faced) {   // face rows tiled per macro face, edge / vertex rows below
-    const int4 *ft = reinterpret_cast<const int4 *>(s->face_tiles);
     const int nb = (int)s->nface_tiles, nt = FACE_TA * FACE_TB;
     const bool mixed = s->pfac != nullptr;
+    if (!s->face_k || !s->face_g) return HHG_ERR_ARG;
     if (res) {
-      if (mixed) surface_face_kernel<true, true><<<nb, nt, 0, S(stream)>>>(G, s->faces, ft, out, push);
-      else surface_face_kernel<true, false><<<nb, nt, 0, S(stream)>>>(G, s->faces, ft, out, push);
+      if (mixed) surface_face_kernel<true, true><<<nb, nt, 0, S(stream)>>>(G, *s, out, push);
+      else surface_face_kernel<true, false><<<nb, nt, 0, S(stream)>>>(G, *s, out, push);
     } else {
-      if (mixed) surface_face_kernel<false, true><<<nb, nt, 0, S(stream)>>>(G, s->faces, ft, out, push);
-      else surface_face_kernel<false, false><<<nb, nt, 0, S(stream)>>>(G, s->faces, ft, out, push);
+      if (mixed) surface_face_kernel<false, true><<<nb, nt, 0, S(stream)>>>(G, *s, out, push);
+      else surface_face_kernel<false, false><<<nb, nt, 0, S(stream)>>>(G, *s, out, push);
     }
     int rc = check("surface_face_kernel");
     if (rc) return rc;

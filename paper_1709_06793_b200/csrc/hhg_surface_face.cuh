@@ -1,4 +1,4 @@
-// Face rows of the surface, tiled per macro face (the default apply path).
+// Face rows of the surface, tiled per macro face.
 //
 // A free macro-face point's row is the sum, over the (one or two) incident
 // macro elements in ascending element order, of the one-sided partial
@@ -6,14 +6,17 @@
 // hhg_surface.cuh).  Instead of one thread per stored incidence (two passes
 // through a partial-sum array) or the precomputed weights of
 // surface_csr_kernel (~400 B per row), one thread owns one face point and
-// forms both partial rows from the lattices directly: the point's
-// coordinates in each incident element are affine in the face-local (a, b)
-// (host-built per face: hhg_face), neighbours come from the element's volume
-// block / ghost shell and coefficient lattice (inc_gather).  Tiles are 32 x 8
-// face points, a running along the fastest lattice direction of the first
-// element, so its reads are coalesced and the second element's cover a
-// compact parallelogram.  Same IEEE operations and order as the other two
-// surface paths: results are bitwise theirs.
+// forms both partial rows from three face-parallel layers: the face itself
+// and each incident element's lattice layer next to it, indexed by the
+// face-local (a, b) of the reference's face numbering.  The coefficients of
+// those layers never change, so they (and the global id of every layer
+// point) are stored once per face in face-local order (hhg_surface.face_k /
+// face_g); an apply streams them and gathers u through the ids.  A CTA owns
+// 32 x 8 face points: it stages the three layers over the tile plus a
+// one-point halo into shared memory, then every thread forms its row
+// through the per-face direction -> layer offset table.  Same IEEE
+// operations and order as the other two surface paths: results are bitwise
+// theirs.
 //
 // Rows on macro edges and vertices (few) stay on surface_csr_kernel through
 // a row sub-list.
@@ -24,39 +27,63 @@
 namespace hhg {
 
 constexpr int FACE_TA = 32, FACE_TB = 8;   // face tile: 32 (a) x 8 (b) points
+constexpr int FACE_W = FACE_TA + 2, FACE_H = FACE_TB + 2;   // staged region (halo 1)
 
 template <bool RES, bool MIXED>
 __global__ void __launch_bounds__(FACE_TA * FACE_TB)
-surface_face_kernel(SurfGSDesc G, const hhg_face *faces, const int4 *tiles, double *out,
-                    SurfPush push) {
+surface_face_kernel(SurfGSDesc G, const hhg_surface s, double *out, SurfPush push) {
+  // layer 0: the face points (shared by both elements); layer 1 + e: the
+  // layer of element e next to the face; (v, k) pairs over the tile + halo
+  constexpr int AREA = FACE_H * FACE_W;
+  __shared__ double2 Ls[3 * AREA];
+  __shared__ hhg_face F;
+  __shared__ int offs[2][14];      // direction -> Ls offset relative to the point
+  constexpr int NONE = -(1 << 20);   // direction leaving the element
   const SurfDesc &D = G.s;
-  const int4 tl = tiles[blockIdx.x];
-  const hhg_face &F = faces[tl.x];
-  const int n = D.n;
-  const int a = tl.y + (threadIdx.x % FACE_TA), b = tl.z + (threadIdx.x / FACE_TA);
-  if (a < 1 || b < 1 || a + b > n - 1) return;
-  double row = 0.0, v0 = 0.0;
-  long long gid = 0;
-#pragma unroll
-  for (int e = 0; e < 2; ++e) {
-    const int t = F.tet[e];
-    if (t < 0) break;
-    const int i = F.c[e][0] + F.A[e][0] * a + F.A[e][1] * b;
-    const int j = F.c[e][1] + F.A[e][2] * a + F.A[e][3] * b;
-    const int k = F.c[e][2] + F.A[e][4] * a + F.A[e][5] * b;
-    const int cls = F.cls[e];
-    const unsigned mask = c_cls_dirmask[cls];
-    if (e == 0) {
-      const IncPlanes P = inc_planes(n, k);
-      int off;
-      inc_voff(P, 1, n, i, j, k, off);            // a boundary point: shell offset
-      const long long s = (long long)t * D.S + off;
-      v0 = D.ghost[s];
-      gid = G.shell_gid[s];
+  const int4 tl = reinterpret_cast<const int4 *>(s.face_tiles)[blockIdx.x];
+  if (threadIdx.x < sizeof(hhg_face) / 4)
+    reinterpret_cast<int *>(&F)[threadIdx.x] =
+        reinterpret_cast<const int *>(s.faces + tl.x)[threadIdx.x];
+  __syncthreads();
+  const int n = D.n, a0 = tl.y, b0 = tl.z, sq = s.face_sq;
+  const int ne = F.tet[1] >= 0 ? 2 : 1;
+  if (threadIdx.x < 28) {
+    const int e = threadIdx.x / 14, d = threadIdx.x % 14;
+    const int l = F.dl[e][d];
+    offs[e][d] = l < 0 ? NONE : (l == 0 ? 0 : 1 + e) * AREA + F.db[e][d] * FACE_W + F.da[e][d];
+  }
+  // stage: static k and global ids of the layers, u gathered through them
+  const long long layer0 = (long long)tl.x * 3 * sq * sq;
+  for (int x = threadIdx.x; x < (1 + ne) * AREA; x += blockDim.x) {
+    const int l = x / AREA, rem = x - l * AREA;
+    const int rb = rem / FACE_W, ra = rem - rb * FACE_W;
+    // square index of (a, b) = (a0 - 1 + ra, b0 - 1 + rb): (b + 1) sq + a + 1
+    if (a0 + ra >= sq || b0 + rb >= sq) {      // past the face's (n+3)^2 square
+      Ls[x] = make_double2(0.0, 0.0);
+      continue;
     }
+    const long long idx = layer0 + (long long)l * sq * sq + (long long)(b0 + rb) * sq + (a0 + ra);
+    const double kv = __ldg(s.face_k + idx);
+    const double v = __ldg(D.u + (unsigned)__ldg(s.face_g + idx));
+    Ls[x] = make_double2(v, kv);
+  }
+  __syncthreads();
+  const int ta = threadIdx.x % FACE_TA, tb = threadIdx.x / FACE_TA;
+  const int a = a0 + ta, b = b0 + tb;
+  if (a < 1 || b < 1 || a + b > n - 1) return;
+  const int ctr = (tb + 1) * FACE_W + (ta + 1);
+  const double2 c0 = Ls[ctr];
+  const double v0 = c0.x;
+  double row = 0.0;
+  for (int e = 0; e < ne; ++e) {
+    const int t = F.tet[e], cls = F.cls[e];
+    const unsigned mask = c_cls_dirmask[cls];
     double2 q[14];
-    double k0;
-    inc_gather(D, t, i, j, k, mask, v0, q, k0);
+#pragma unroll
+    for (int d = 0; d < 14; ++d) {
+      const int o = offs[e][d];
+      q[d] = o == NONE ? make_double2(v0, 0.0) : Ls[ctr + o];
+    }
     double part;
     if (!MIXED || !F.nodal) {
       const double *sh = D.psh + ((long long)t * 14 + cls) * 14;
@@ -64,17 +91,21 @@ surface_face_kernel(SurfGSDesc G, const hhg_face *faces, const int4 *tiles, doub
 #pragma unroll
       for (int d = 0; d < 14; ++d)
         if (mask >> d & 1)
-          part = dadd(part, dmul(dmul(dadd(k0, q[d].y), __ldg(sh + d)), dsub(q[d].x, v0)));
+          part = dadd(part, dmul(dmul(dadd(c0.y, q[d].y), __ldg(sh + d)), dsub(q[d].x, v0)));
     } else {
       const double *fac = D.pfac + ((long long)t * 14 + cls) * 72;
-      part = nodal_row_exact(v0, k0, q, fac);
+      part = nodal_row_exact(v0, c0.y, q, fac);
     }
     row = dadd(row, part);
   }
+  // interior face points are numbered fs + base2(b - 1) + a - 1 (face-local
+  // (a, b) = the barycentrics of the face's 2nd and 3rd sorted vertices)
+  const long long off = (long long)(b - 1) * (n - 2) - (long long)(b - 1) * (b - 2) / 2 + a - 1;
+  const long long gid = F.fs + off;
   if (RES) row = dsub(D.f[gid], row);
   out[gid] = row;
   if (!RES && push.slot) {
-    const int sl = __ldg(push.slot + (F.rbase + (gid - F.fs)));
+    const int sl = __ldg(push.slot + (F.rbase + off));
     if (sl >= 0) {
       if (sl < push.split) push.dst0[sl] = row;
       else push.dst1[sl - push.split] = row;

@@ -220,28 +220,72 @@ class SurfaceTables:
 
 FACE_TA, FACE_TB = 32, 8     # face tile of surface_face_kernel (hhg_surface_face.cuh)
 
-# (i, j, k) = c + A (a, b) on the face opposite local vertex f (barycentric
-# slot f = 0 is n - i - j - k, slots 1..3 are i, j, k), a along the fastest
-# lattice direction available on that face
-_FACE_PATTERN = {3: ((1, 0, 0, 1, 0, 0), (0, 0, 0)),     # k = 0: (a, b, 0)
-                 2: ((1, 0, 0, 0, 0, 1), (0, 0, 0)),     # j = 0: (a, 0, b)
-                 1: ((0, 0, 1, 0, 0, 1), (0, 0, 0)),     # i = 0: (0, a, b)
-                 0: ((1, 0, 0, 1, -1, -1), None)}        # i+j+k = n: (a, b, n-a-b)
+
+def _face_layers(A, cls):
+    """Where each stencil direction of a face point lands in the face-local
+    layers of one incident element: (nb, dl[14], da[14], db[14]) with nb the
+    offset of the inner layer (re-centred so that every offset is in
+    [-1, 1]), dl 0 = face layer, 1 = inner layer, -1 = outside the element,
+    and (da, db) the face-local offset within that layer."""
+    from .reference_stencils import class_element_masks
+    _, inside = class_element_masks()
+    M = np.array([[A[0], A[1]], [A[2], A[3]], [A[4], A[5]]], dtype=np.float64)
+
+    def solve(v):
+        xy = np.rint(np.linalg.lstsq(M, np.asarray(v, dtype=np.float64), rcond=None)[0])
+        return (int(xy[0]), int(xy[1])) if np.array_equal(M @ xy, v) else None
+
+    dl, da, db = [-1] * 14, [0] * 14, [0] * 14
+    nb = None
+    for d in range(14):
+        if not inside[cls, d]:
+            continue
+        xy = solve(DIRS_3D[d])
+        if xy is not None:
+            dl[d], (da[d], db[d]) = 0, xy
+            continue
+        if nb is None:
+            nb = tuple(int(x) for x in DIRS_3D[d])
+        xy = solve(np.asarray(DIRS_3D[d]) - np.asarray(nb))
+        if xy is None:
+            raise AssertionError("inner stencil direction not on the inner layer")
+        dl[d], (da[d], db[d]) = 1, xy
+    if nb is None:
+        raise AssertionError("face class without inner directions")
+    inner = [d for d in range(14) if dl[d] == 1]
+    sa = (min(da[d] for d in inner) + max(da[d] for d in inner)) // 2
+    sb = (min(db[d] for d in inner) + max(db[d] for d in inner)) // 2
+    for d in inner:
+        da[d] -= sa
+        db[d] -= sb
+    nb = tuple(int(x) for x in np.asarray(nb) + M.astype(np.int64) @ np.array([sa, sb]))
+    if max(abs(x) for x in da + db) > 1:
+        raise AssertionError("unexpected face stencil geometry")
+    return nb, tuple(dl), tuple(da), tuple(db)
 
 
 class FaceTables:
-    """Free macro faces for the face-tiled surface kernel: per face its
-    incident elements in ascending order, the boundary class of the face in
-    each, the affine maps face-local (a, b) -> element lattice (i, j, k), the
-    global id / row index of its first interior point; the 32 x 8 tiles; and
-    the remaining surface rows (macro edges and vertices) as a sub-list."""
+    """Free macro faces for the face-tiled surface kernel.
 
-    def __init__(self, grid, gt: GridTables, st: SurfaceTables):
+    Face-local coordinates (a, b) are the barycentrics of the face's second
+    and third (sorted) global vertices, so the interior points of face F are
+    the global ids face_start[F] + base2(b - 1) + a - 1 (the reference's face
+    numbering, mesh.py:654-701).  Per face: its incident elements in
+    ascending order with the face's boundary class in each, the affine maps
+    (a, b) -> element lattice (i, j, k), the direction table of each
+    element; and static layers over (a, b) in [-1, n+1]^2 - the face points
+    and each element's layer next to the face: coefficient and global id of
+    every lattice point (k never changes, so the kernel gathers only u).
+    The remaining surface rows (macro edges and vertices) form a sub-list."""
+
+    def __init__(self, grid, gt: GridTables, st: SurfaceTables, kc_values):
         n = grid.n
         m = grid.macro
         rows = np.asarray(st.rows)
         npf = grid.nodes_per_face
-        recs, tiles = [], []
+        sq = n + 3
+        self.sq = sq
+        recs, tiles, ks, gs = [], [], [], []
         covered = np.zeros(len(rows), dtype=bool)
         inc = [[] for _ in range(len(m.faces))]
         if n >= 4:
@@ -249,6 +293,8 @@ class FaceTables:
                 for f in range(4):
                     inc[int(m.elem_faces[t, f])].append((t, f))
         lat = grid.lat
+        aa, bb = np.meshgrid(np.arange(-1, n + 2), np.arange(-1, n + 2))   # [b, a]
+        aa, bb = aa.ravel(), bb.ravel()
         for F, tf in enumerate(inc):
             if not tf or len(tf) > 2:
                 continue
@@ -257,40 +303,40 @@ class FaceTables:
             if r0 + npf > len(rows) or rows[r0] != fs or rows[r0 + npf - 1] != fs + npf - 1:
                 continue                      # Dirichlet face (no rows) or not a plain block
             tf = sorted(tf)
-            A, c, cls = [], [], []
-            t1, f1 = tf[0]
-            a1, c1 = _FACE_PATTERN[f1]
-            c1 = c1 if c1 is not None else (0, 0, n)
+            gA, gB, gC = (int(x) for x in m.faces[F])
+            A, c, cls, lay = [], [], [], []
+            kl = np.zeros((3, sq * sq))
+            gl = np.zeros((3, sq * sq), dtype=np.int32)
             for e, (t, f) in enumerate(tf):
+                conn = [int(x) for x in m.elements[t]]
+                # barycentric slot s of local vertex s: 0 -> n-i-j-k, 1..3 -> i, j, k
+                coef = np.zeros((4, 3), dtype=np.int64)       # slot value = coef @ (a, b, 1)
+                coef[conn.index(gA)] = (-1, -1, n)
+                coef[conn.index(gB)] = (1, 0, 0)
+                coef[conn.index(gC)] = (0, 1, 0)
+                Ae = tuple(int(x) for x in coef[1:, :2].ravel())   # (ia, ib, ja, jb, ka, kb)
+                ce = tuple(int(x) for x in coef[1:, 2])
+                A.append(Ae)
+                c.append(ce)
                 cls.append(CLASS_OF_MASK[1 << f])
-                if e == 0:
-                    A.append(a1)
-                    c.append(c1)
-                    continue
-                pts = []
-                for (pa, pb) in ((1, 1), (2, 1), (1, 2), (n - 2, 1), (1, n - 2)):
-                    i = c1[0] + a1[0] * pa + a1[1] * pb
-                    j = c1[1] + a1[2] * pa + a1[3] * pb
-                    k = c1[2] + a1[4] * pa + a1[5] * pb
-                    gid = grid.elem_gidx[t1, lat.base[k, j] + i]
-                    pos = np.nonzero(gt.shell_gid[t] == gid)[0]
-                    if len(pos) != 1:
-                        raise AssertionError("face point not on the neighbour's shell")
-                    pts.append(lat.coords[gt.shell_pos[pos[0]]].astype(np.int64))
-                p11, p21, p12 = pts[:3]
-                da, db = p21 - p11, p12 - p11
-                cc = p11 - da - db
-                for (pa, pb), p in zip(((n - 2, 1), (1, n - 2)), pts[3:]):
-                    if not np.array_equal(cc + da * pa + db * pb, p):
-                        raise AssertionError("face map is not affine")
-                A.append((int(da[0]), int(db[0]), int(da[1]), int(db[1]), int(da[2]),
-                          int(db[2])))
-                c.append(tuple(int(x) for x in cc))
-            recs.append((tuple(x for x, _ in tf) + ((-1,) if len(tf) == 1 else ()),
-                         tuple(cls) + ((0,) if len(tf) == 1 else ()),
-                         tuple(A) + (((0,) * 6,) if len(tf) == 1 else ()),
-                         tuple(c) + (((0, 0, 0),) if len(tf) == 1 else ()),
-                         int(st.row_nodal[r0]), fs, r0))
+                lay.append(_face_layers(Ae, cls[-1]))
+                for l, off in ((0, (0, 0, 0)), (1 + e, lay[-1][0])) if e == 0 else \
+                        ((1 + e, lay[-1][0]),):
+                    i = ce[0] + off[0] + Ae[0] * aa + Ae[1] * bb
+                    j = ce[1] + off[1] + Ae[2] * aa + Ae[3] * bb
+                    k = ce[2] + off[2] + Ae[4] * aa + Ae[5] * bb
+                    ok = (i >= 0) & (j >= 0) & (k >= 0) & (i + j + k <= n)
+                    flat = lat.base[np.where(ok, k, 0), np.where(ok, j, 0)] + np.where(ok, i, 0)
+                    kl[l] = np.where(ok, kc_values[t][flat], 0.0)
+                    gl[l] = np.where(ok, grid.elem_gidx[t, flat], 0)
+            if len(tf) == 1:
+                t_, cls_, A_, c_ = (tf[0][0], -1), (cls[0], 0), (A[0], (0,) * 6), (c[0], (0,) * 3)
+                lay.append(((0, 0, 0), (-1,) * 14, (0,) * 14, (0,) * 14))
+            else:
+                t_, cls_, A_, c_ = tuple(x for x, _ in tf), tuple(cls), tuple(A), tuple(c)
+            recs.append((t_, cls_, A_, c_, tuple(lay), int(st.row_nodal[r0]), fs, r0))
+            ks.append(kl)
+            gs.append(gl)
             covered[r0:r0 + npf] = True
             fid = len(recs) - 1
             for b0 in range(1, n - 1, FACE_TB):
@@ -299,19 +345,28 @@ class FaceTables:
         self.faces = recs
         self.tiles = np.ascontiguousarray(np.array(tiles, dtype=np.int32).reshape(-1, 4))
         self.sub_rows = np.ascontiguousarray(np.nonzero(~covered)[0].astype(np.int32))
+        self.layer_k = np.ascontiguousarray(np.stack(ks)) if ks else np.zeros((0, 3, sq * sq))
+        self.layer_g = np.ascontiguousarray(np.stack(gs)) if gs else \
+            np.zeros((0, 3, sq * sq), dtype=np.int32)
+        if grid.n_nodes >= 2 ** 31:
+            raise ValueError("face-tiled surface rows use 32-bit global ids")
 
     def packed(self):
         """The faces as an array of hhg_face structs (bytes)."""
         from ._lib import HhgFace
         arr = (HhgFace * max(len(self.faces), 1))()
-        for x, (tet, cls, A, c, nodal, fs, rb) in enumerate(self.faces):
+        for x, (tet, cls, A, c, lay, nodal, fs, rb) in enumerate(self.faces):
             h = arr[x]
             for e in range(2):
                 h.tet[e], h.cls[e] = tet[e], cls[e]
                 for q in range(6):
                     h.A[e][q] = A[e][q]
+                nb, dl, da, db = lay[e]
                 for q in range(3):
                     h.c[e][q] = c[e][q]
+                    h.nb[e][q] = nb[q]
+                for d in range(14):
+                    h.dl[e][d], h.da[e][d], h.db[e][d] = dl[d], da[d], db[d]
             h.nodal, h.fs, h.rbase = nodal, fs, rb
         return np.frombuffer(bytes(arr), dtype=np.uint8).copy()
 
@@ -404,6 +459,11 @@ class DeviceSurface:
             d.face_tiles = self.face_tiles.data_ptr()
             d.nsub = len(faces.sub_rows)
             d.sub_rows = self.sub_rows.data_ptr()
+            self.layer_k = t(faces.layer_k.reshape(-1))
+            self.layer_g = t(faces.layer_g.reshape(-1))
+            d.face_k = self.layer_k.data_ptr()
+            d.face_g = self.layer_g.data_ptr()
+            d.face_sq = faces.sq
         self.desc = d
         self.ref = ctypes.byref(d)
         self._levels = None

@@ -61,7 +61,7 @@ class Operator:
     """One operator variant bound to a grid and coefficient, on the GPU."""
 
     def __init__(self, grid, variant: str, coeff=None, hybrid_nodal=frozenset(),
-                 fast=False, surface_mode="csr"):
+                 fast=False, surface_mode="face"):
         if variant not in VARIANTS:
             raise ValueError(f"unknown variant {variant!r}")
         if variant == "stored":
@@ -211,8 +211,8 @@ class Operator:
                 kc = self.coeff.values
             dg = DeviceGrid(gt, kc)
             st = SurfaceTables(grid, gt, self._nodal_kinds)
-            faces = FaceTables(grid, gt, st) if (self.surface_mode == "face" and
-                                                 not self.is_tensor) else None
+            faces = FaceTables(grid, gt, st, kc) if (self.surface_mode == "face" and
+                                                     not self.is_tensor) else None
             ds = DeviceSurface(st, self._psh, self._pfac,
                                tensor=(self.coeff.M, km) if self.is_tensor else None,
                                faces=faces)
@@ -356,8 +356,11 @@ class Operator:
         return out
 
     def _surface(self, dg, ds, res_flag, du, fp, out, st, push=None):
-        """Surface + Dirichlet rows: from the precomputed rows when built
-        (setup on first use, `surface_mode="csr"`), else matrix-free.
+        """Surface + Dirichlet rows.  ``surface_mode``: "face" (default) -
+        face rows by the face-tiled kernel from static face-major layers,
+        edge / vertex rows from the precomputed rows; "csr" - every row from
+        the precomputed rows (filled on the device on first use); or
+        "matrix-free" (two passes over the incidences).  Bitwise equal.
         ``push`` = (slot_ptr, dst0, dst1, split): also store the interface
         rows into the neighbours' receive buffers (shard.PeerExchange)."""
         if self.surface_mode != "matrix-free":

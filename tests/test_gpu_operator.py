@@ -276,10 +276,11 @@ def test_large_grid_algebraic_properties(cuda):
 @pytest.mark.parametrize("name", ["scaling", "nodal", "hybrid:wv+we", "hybrid:wf"])
 @pytest.mark.parametrize("cfg", ["c3", "c5"])
 def test_surface_modes_agree_bitwise(cuda, name, cfg):
-    """The three executions of the surface rows - precomputed rows for every
-    row (default), face-tiled (face rows per macro face, edge / vertex rows
-    from the precomputed rows) and the matrix-free two-pass kernels -
-    perform the same IEEE operations in the same order."""
+    """The three executions of the surface rows - face-tiled (default: face
+    rows per macro face from static face-major layers, edge / vertex rows
+    from the precomputed rows), precomputed rows for every row, and the
+    matrix-free two-pass kernels - perform the same IEEE operations in the
+    same order."""
     grid = M.RefinedGrid(case_mesh(cfg), 4)
     kf = sample_nodal(k_c3(), grid)
     hn, v = frozenset(), name
@@ -287,11 +288,11 @@ def test_surface_modes_agree_bitwise(cuda, name, cfg):
         hn, v = parse_hybrid_set(name.split(":", 1)[1]), "hybrid"
     u = np.random.default_rng(9).uniform(-1, 1, grid.n_nodes)
     f = np.random.default_rng(10).uniform(-1, 1, grid.n_nodes)
-    a = Operator(grid, v, kf, hybrid_nodal=hn, surface_mode="face")
+    a = Operator(grid, v, kf, hybrid_nodal=hn)                      # default: face-tiled
     ds = a._device()["surf"]
     assert ds.desc.nfaces > 0 and ds.desc.nsub < len(ds.st.rows)
     b = Operator(grid, v, kf, hybrid_nodal=hn, surface_mode="matrix-free")
-    c = Operator(grid, v, kf, hybrid_nodal=hn)         # every row from the precomputed rows
+    c = Operator(grid, v, kf, hybrid_nodal=hn, surface_mode="csr")  # every row precomputed
     assert c._device()["surf"].desc.nfaces == 0
     for x in (b, c):
         assert np.array_equal(a.apply(u), x.apply(u))
@@ -575,7 +576,7 @@ def test_config5_slab_whole_vector_against_oracle(cuda, fast):
 
 
 @pytest.mark.parametrize("cfg,variant,kw", [("c3", "scaling", {}), ("c3", "scaling", {"fast": True}),
-                                            ("c5", "scaling", {"surface_mode": "face"}),
+                                            ("c5", "scaling", {"surface_mode": "csr"}),
                                             ("c3", "nodal", {}),
                                             ("c3", "scaling", {"surface_mode": "matrix-free"})])
 def test_no_writes_outside_the_output(cuda, cfg, variant, kw):
