@@ -257,6 +257,36 @@ int hhg_csr_spmv(int64_t nrows, const int64_t *indptr, const int64_t *indices,
                  const double *data, const double *x, double *y, int accumulate,
                  void *stream);
 
+/* grid transfers between levels l-1 (coarse) and l (fine) of one macro
+ * mesh (multigrid.py:23-77, 130-138), lattice-native: volume rows in
+ * closed form from the element lattices, the rows of surface nodes (macro
+ * vertices / edges / faces) from small host-built CSRs with a row list */
+typedef struct hhg_transfer {
+  int32_t nf, nc;              /* fine / coarse 2^level                          */
+  int32_t ntets, pad_;
+  const int64_t *f_vol_start;  /* [ntets] fine volume blocks                     */
+  const int64_t *c_vol_start;  /* [ntets] coarse volume blocks                   */
+  const int64_t *c_shell_gid;  /* [ntets * c_shell_size] coarse ghost-shell ids  */
+  int64_t c_shell_size;
+  /* P rows of the fine surface nodes: y[p_rows[r]] = sum p_val x[p_col]     */
+  int64_t p_nrows;
+  const int64_t *p_rows, *p_ptr, *p_col;
+  const double *p_val;
+  /* P^T rows of the coarse surface nodes (children in ascending fine id)   */
+  int64_t r_nrows;
+  const int64_t *r_rows, *r_ptr, *r_col;
+  const double *r_val;
+  int64_t ndir;                /* coarse Dirichlet ids, zeroed by the restriction */
+  const int64_t *c_dir_ids;
+} hhg_transfer;
+
+/* yf = P xc (accumulate != 0: yf += P xc), bitwise the reference's P @ x */
+int hhg_prolongate(const hhg_transfer *T, const double *xc, double *yf, int accumulate,
+                   void *stream);
+/* yc = P^T xf with the coarse Dirichlet rows zeroed, bitwise the
+ * reference's restrict (P.T @ r, then r[dirichlet] = 0) */
+int hhg_restrict(const hhg_transfer *T, const double *xf, double *yc, void *stream);
+
 /* y[ids[e]] = 0 (coarse Dirichlet rows after restriction) */
 int hhg_scatter_zero(int64_t n, const int64_t *ids, double *y, void *stream);
 

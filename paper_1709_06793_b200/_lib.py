@@ -10,7 +10,8 @@ import ctypes
 import os
 from pathlib import Path
 
-__all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "HhgSurfaceGS", "HhgFace", "check",
+__all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "HhgSurfaceGS", "HhgFace", "HhgTransfer",
+           "check",
            "HhgError",
            "VAR", "FLAG_RESIDUAL", "FLAG_FAST", "FLAG_MIRROR", "EXPORTS"]
 
@@ -48,6 +49,18 @@ class HhgSurface(ctypes.Structure):
                 ("face_tiles", vp), ("nsub", ctypes.c_int64), ("sub_rows", vp),
                 ("face_k", vp), ("face_g", vp), ("face_sq", ctypes.c_int32),
                 ("pad_", ctypes.c_int32)]
+
+
+class HhgTransfer(ctypes.Structure):
+    _fields_ = [("nf", ctypes.c_int32), ("nc", ctypes.c_int32),
+                ("ntets", ctypes.c_int32), ("pad_", ctypes.c_int32),
+                ("f_vol_start", vp), ("c_vol_start", vp), ("c_shell_gid", vp),
+                ("c_shell_size", ctypes.c_int64),
+                ("p_nrows", ctypes.c_int64), ("p_rows", vp), ("p_ptr", vp), ("p_col", vp),
+                ("p_val", vp),
+                ("r_nrows", ctypes.c_int64), ("r_rows", vp), ("r_ptr", vp), ("r_col", vp),
+                ("r_val", vp),
+                ("ndir", ctypes.c_int64), ("c_dir_ids", vp)]
 
 
 class HhgFace(ctypes.Structure):
@@ -149,6 +162,8 @@ EXPORTS = {
     "hhg_dot_masked": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp]),
     "hhg_csr_spmv": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp,
                                     ctypes.c_int, vp]),
+    "hhg_prolongate": (ctypes.c_int, [ctypes.POINTER(HhgTransfer), vp, vp, ctypes.c_int, vp]),
+    "hhg_restrict": (ctypes.c_int, [ctypes.POINTER(HhgTransfer), vp, vp, vp]),
     "hhg_scatter_zero": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp]),
     "hhg_status": (ctypes.c_int, []),
     "hhg_status_reset": (ctypes.c_int, []),

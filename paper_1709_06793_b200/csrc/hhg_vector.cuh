@@ -3,6 +3,7 @@
 // CG iteration), and CSR products for the grid transfers.
 #pragma once
 #include "hhg_common.cuh"
+#include "hhg_transfer.cuh"
 
 namespace hhg {
 
@@ -167,6 +168,19 @@ __global__ void csr_spmv_kernel(long long nrows, const long long *indptr,
   y[r] = accumulate ? dadd(y[r], s) : s;
 }
 
+// rows r of a row-listed CSR: y[rows[r]] (+)= sum_e val[e] x[col[e]] in
+// stored order (the surface rows of the grid transfers)
+__global__ void csr_rows_kernel(long long nrows, const long long *rows, const long long *ptr,
+                                const long long *col, const double *val, const double *x,
+                                double *y, int accumulate) {
+  const long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  double s = 0.0;
+  for (long long e = ptr[r]; e < ptr[r + 1]; ++e) s = dadd(s, dmul(val[e], x[col[e]]));
+  const long long g = rows[r];
+  y[g] = accumulate ? dadd(y[g], s) : s;
+}
+
 __global__ void scatter_zero_kernel(long long n, const long long *ids, double *y) {
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e < n) y[ids[e]] = 0.0;
@@ -269,6 +283,48 @@ int hhg_csr_spmv(int64_t nrows, const int64_t *indptr, const int64_t *indices,
       nrows, reinterpret_cast<const long long *>(indptr),
       reinterpret_cast<const long long *>(indices), data, x, y, accumulate);
   return check("vector kernel");
+}
+
+int hhg_prolongate(const hhg_transfer *T, const double *xc, double *yf, int accumulate,
+                   void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (T->nf >= 4 && T->ntets > 0) {
+    hhg::prolong_volume_kernel<<<dim3(T->nf - 3, T->ntets), 256, 0, st>>>(*T, xc, yf,
+                                                                          accumulate);
+    int rc = check("prolong_volume_kernel");
+    if (rc) return rc;
+  }
+  if (T->p_nrows > 0) {
+    hhg::csr_rows_kernel<<<(int)((T->p_nrows + 255) / 256), 256, 0, st>>>(
+        T->p_nrows, reinterpret_cast<const long long *>(T->p_rows),
+        reinterpret_cast<const long long *>(T->p_ptr),
+        reinterpret_cast<const long long *>(T->p_col), T->p_val, xc, yf, accumulate);
+    return check("csr_rows_kernel");
+  }
+  return HHG_OK;
+}
+
+int hhg_restrict(const hhg_transfer *T, const double *xf, double *yc, void *stream) {
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (T->nc >= 4 && T->ntets > 0) {
+    hhg::restrict_volume_kernel<<<dim3(T->nc - 3, T->ntets), 128, 0, st>>>(*T, xf, yc);
+    int rc = check("restrict_volume_kernel");
+    if (rc) return rc;
+  }
+  if (T->r_nrows > 0) {
+    hhg::csr_rows_kernel<<<(int)((T->r_nrows + 255) / 256), 256, 0, st>>>(
+        T->r_nrows, reinterpret_cast<const long long *>(T->r_rows),
+        reinterpret_cast<const long long *>(T->r_ptr),
+        reinterpret_cast<const long long *>(T->r_col), T->r_val, xf, yc, 0);
+    int rc = check("csr_rows_kernel");
+    if (rc) return rc;
+  }
+  if (T->ndir > 0) {
+    hhg::scatter_zero_kernel<<<(int)((T->ndir + 255) / 256), 256, 0, st>>>(
+        T->ndir, reinterpret_cast<const long long *>(T->c_dir_ids), yc);
+    return check("scatter_zero_kernel");
+  }
+  return HHG_OK;
 }
 
 int hhg_scatter_zero(int64_t n, const int64_t *ids, double *y, void *stream) {
