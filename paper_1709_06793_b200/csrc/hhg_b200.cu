@@ -354,8 +354,33 @@ static int device_capacity(K kern, int threads, std::map<int, int> &cache) {
   return cap;
 }
 
+#ifndef HHG_GS_CLUSTER
+#define HHG_GS_CLUSTER 8         // CTAs per element of the cluster sweep (0: off)
+#endif
+
 template <int VAR>
 static int launch_gs_volume(GSDesc G, cudaStream_t st) {
+  if (HHG_GS_CLUSTER > 0 && G.n >= 16) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G.ntets * HHG_GS_CLUSTER);
+    cfg.blockDim = dim3(gs_cluster_threads<VAR>());
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = HHG_GS_CLUSTER;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    G.cpt = HHG_GS_CLUSTER;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gs_volume_cluster_kernel<VAR>, G);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "hhg_b200: gs_volume_cluster_kernel: %s\n", cudaGetErrorString(e));
+      return HHG_ERR_CUDA;
+    }
+    return HHG_OK;
+  }
   static std::map<int, int> caps;
   const int capacity = device_capacity(gs_volume_kernel<VAR, true>,
                                        gs_volume_threads<VAR, true>(), caps);

@@ -181,6 +181,162 @@ gs_volume_kernel(GSDesc D) {
   }
 }
 
+// Cluster form of the volume sweep: one thread-block cluster of CL CTAs per
+// macro element (elements are independent given their ghost shells, so no
+// grid-wide barrier is needed - clusters of different elements run and
+// finish independently), a hardware cluster barrier (release / acquire,
+// cluster scope) between hyperplanes, values written by other CTAs of the
+// cluster read through L2 (ld.global.cg).  Each thread takes its points of
+// a hyperplane two at a time and issues both points' neighbour loads before
+// either update, so twice the loads are in flight; the static part of the
+// next hyperplane's first pair (k values, f, point code) is loaded before
+// the barrier.  Same point set per hyperplane, same arithmetic: bitwise the
+// lexicographic sweep.
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ unsigned cluster_ctarank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cluster_nctas() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
+  return r;
+}
+
+#ifndef HHG_GS_CT
+#define HHG_GS_CT 128            // threads per CTA of the cluster sweep (scaling)
+#endif
+#ifndef HHG_GS_PRELOAD
+#define HHG_GS_PRELOAD 1         // static part of the next pair loaded before the barrier
+#endif
+template <int VAR>
+constexpr int gs_cluster_threads() { return VAR == 0 ? HHG_GS_CT : 128; }
+
+template <int VAR>
+__global__ void __launch_bounds__(gs_cluster_threads<VAR>())
+gs_volume_cluster_kernel(GSDesc D) {
+  const int cpt = (int)cluster_nctas();
+  const int t = blockIdx.x / cpt;
+  const int part = (int)cluster_ctarank();
+  const int n = D.n;
+  __shared__ double sfac[72];
+  double coef[14];
+  if (VAR == 0) {
+#pragma unroll
+    for (int d = 0; d < 14; ++d) coef[d] = D.coef[(long long)t * D.coef_stride + d];
+  } else {
+    for (int e = threadIdx.x; e < 72; e += blockDim.x)
+      sfac[e] = D.coef[(long long)t * D.coef_stride + e];
+    __syncthreads();
+  }
+  const double omega = D.omega;
+  const int hmin = 6, hmax = 3 * n - 6;
+  const double *kt = D.kc + (long long)t * D.L;
+  const int stride = cpt * blockDim.x;
+  const int first = part * blockDim.x + threadIdx.x;
+  double *ut = D.u + D.vol_start[t];
+  const double *gt = D.ghost + (long long)t * D.S;
+  const double *ft = D.f + D.vol_start[t];
+
+  struct Static {
+    int code;
+    double k0, fv;
+    double kq[14];
+  };
+  auto load_static = [&](int e, Static &S) {
+    S.code = __ldg(D.hp_code + e);
+    const int i = S.code & 1023, j = (S.code >> 10) & 1023, k = (S.code >> 20) & 1023;
+    const IncPlanes P = inc_planes(n, k);
+    S.k0 = __ldg(kt + inc_koff(P, 1, i, j));
+#pragma unroll
+    for (int d = 0; d < 14; ++d)
+      S.kq[d] = __ldg(kt + inc_koff(P, c_dirs_h(d, 2) + 1, i + c_dirs_h(d, 0),
+                                    j + c_dirs_h(d, 1)));
+    S.fv = __ldg(ft + lbase32(n - 4, k - 1, j - 1) + i - 1);
+  };
+  // neighbour values (through L2: other CTAs of the cluster write them)
+  auto gather = [&](const Static &S, double (&qv)[14], int &uoff) {
+    const int i = S.code & 1023, j = (S.code >> 10) & 1023, k = (S.code >> 20) & 1023;
+    const IncPlanes P = inc_planes(n, k);
+    inc_voff(P, 1, n, i, j, k, uoff);                     // interior point
+#pragma unroll
+    for (int d = 0; d < 14; ++d) {
+      const int dk = c_dirs_h(d, 2);
+      int off;
+      const bool in = inc_voff(P, dk + 1, n, i + c_dirs_h(d, 0), j + c_dirs_h(d, 1), k + dk, off);
+      qv[d] = in ? __ldcg(ut + off) : __ldg(gt + off);
+    }
+  };
+  auto finish = [&](const Static &S, const double (&qv)[14], int uoff) {
+    double2 q[14];
+#pragma unroll
+    for (int d = 0; d < 14; ++d) q[d] = make_double2(qv[d], S.kq[d]);
+    double acc = 0.0, diag = 0.0;
+    if (VAR == 0) {
+#pragma unroll
+      for (int d = 0; d < 14; ++d) {
+        const double sd = dmul(dadd(S.k0, q[d].y), coef[d]);
+        acc = dadd(acc, dmul(sd, q[d].x));
+        diag = dsub(diag, sd);
+      }
+    } else {
+      double b[55];
+      nodal_buffer(S.k0, q, b);
+      nodal_gs_terms<0>(acc, diag, q, b, sfac);
+    }
+    if (diag == 0.0) atomicOr(&g_status, 1);
+    const double old = __ldcg(ut + uoff);
+    __stcg(ut + uoff, dadd(dmul(dsub(1.0, omega), old), ddiv(dmul(omega, dsub(S.fv, acc)), diag)));
+  };
+
+  Static pa, pb;
+  int na = 0;              // static points preloaded for the current hyperplane (0..2)
+  auto preload = [&](int h) {
+    const int a = D.hp_ptr[h - hmin], b = D.hp_ptr[h + 1 - hmin];
+    na = 0;
+    if (a + first < b) { load_static(a + first, pa); na = 1; }
+    if (a + first + stride < b) { load_static(a + first + stride, pb); na = 2; }
+  };
+  if (HHG_GS_PRELOAD && hmin <= hmax) preload(hmin);
+  for (int h = hmin; h <= hmax; ++h) {
+    const int hb = D.hp_ptr[h + 1 - hmin];
+    int e = D.hp_ptr[h - hmin] + first;
+    if (!HHG_GS_PRELOAD) {
+      e -= 2 * stride;                  // no preloaded pair: the loop takes them all
+    } else if (na == 2) {
+      double qa[14], qb[14];
+      int oa, ob;
+      gather(pa, qa, oa);
+      gather(pb, qb, ob);
+      finish(pa, qa, oa);
+      finish(pb, qb, ob);
+    } else if (na == 1) {
+      double qa[14];
+      int oa;
+      gather(pa, qa, oa);
+      finish(pa, qa, oa);
+    }
+    for (e += 2 * stride; e < hb; e += 2 * stride) {
+      Static sa, sb;
+      load_static(e, sa);
+      const bool two = e + stride < hb;
+      if (two) load_static(e + stride, sb);
+      double qa[14], qb[14];
+      int oa, ob = 0;
+      gather(sa, qa, oa);
+      if (two) gather(sb, qb, ob);
+      finish(sa, qa, oa);
+      if (two) finish(sb, qb, ob);
+    }
+    if (HHG_GS_PRELOAD && h < hmax) preload(h + 1);
+    cluster_sync_all();
+  }
+}
+
 // --- surface rows, one level per launch -----------------------------------
 struct SurfGSDesc {
   SurfDesc s;
