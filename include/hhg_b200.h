@@ -358,6 +358,15 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s,
                            const double *f, void *stream);
 int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef,
                       double omega, double *u, const double *f, void *stream);
+/* the same volume sweep in a hyperplane-major ("skewed") copy of the
+ * element interiors: u and f are gathered into us / fs (ntets * nvol
+ * doubles each, caller-owned), swept with coalesced accesses, and u is
+ * scattered back; ks is the skewed coefficient from hhg_skew_coefficient
+ * (static per operator).  Bitwise hhg_smooth_volume. */
+int hhg_skew_coefficient(const hhg_grid *g, double *ks, void *stream);
+int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef,
+                           double omega, double *u, const double *f, double *us,
+                           double *fs, const double *ks, void *stream);
 
 /* ---------------------------------------------------------------------
  * (3) tensor-coefficient operators, M = 6 component fields

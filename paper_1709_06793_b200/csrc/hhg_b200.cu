@@ -355,7 +355,7 @@ static int device_capacity(K kern, int threads, std::map<int, int> &cache) {
 }
 
 #ifndef HHG_GS_CLUSTER
-#define HHG_GS_CLUSTER 8         // CTAs per element of the cluster sweep (0: off)
+#define HHG_GS_CLUSTER 4         // CTAs per element of the cluster sweeps (0: off)
 #endif
 
 template <int VAR>
@@ -460,9 +460,10 @@ int hhg_apply_stored_3d(int64_t n, const int64_t *, const double *v, const doubl
 // interior points of each hyperplane h = i + 2j + 3k (host-built once per n)
 struct Hyperplanes {
   int *ptr = nullptr, *code = nullptr;
+  int *start = nullptr;   // [(h - 6) (n + 1) + k]: skewed position of (i, j, k) = start + j
 };
 
-static int hyperplanes(int n, const int **ptr, const int **code) {
+static int hyperplanes(int n, const int **ptr, const int **code, const int **start = nullptr) {
   static std::map<std::pair<int, int>, Hyperplanes> cache;
   std::lock_guard<std::mutex> lock(g_cache_mu);
   const auto key = std::make_pair(current_device(), n);
@@ -479,14 +480,34 @@ static int hyperplanes(int n, const int **ptr, const int **code) {
         }
     }
     if (hmax >= hmin) p[hmax - hmin + 1] = (int)c.size();
+    // skewed (hyperplane-major) position of interior point (i, j, k): its
+    // index in the list above = start[(h - 6)(n + 1) + k] + j
+    std::vector<int> st(std::max(hmax - hmin + 1, 1) * (n + 1), 0);
+    for (int h = hmin; h <= hmax; ++h) {
+      int pos = p[h - hmin];
+      for (int k = 1; k <= n - 3; ++k) {
+        int jmin = -1, cnt = 0;
+        for (int j = 1; j <= n - 2 - k; ++j) {
+          const int i = h - 2 * j - 3 * k;
+          if (i >= 1 && i + j + k <= n - 1) {
+            if (jmin < 0) jmin = j;
+            ++cnt;
+          }
+        }
+        st[(h - hmin) * (n + 1) + k] = jmin < 0 ? 0 : pos - jmin;
+        pos += cnt;
+      }
+    }
     Hyperplanes hp;
     int rc = upload(p, &hp.ptr);
     if (!rc) rc = upload(c, &hp.code);
+    if (!rc) rc = upload(st, &hp.start);
     if (rc) return rc;
     it = cache.emplace(key, hp).first;
   }
   *ptr = it->second.ptr;
   *code = it->second.code;
+  if (start) *start = it->second.start;
   return HHG_OK;
 }
 
@@ -867,6 +888,82 @@ int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef, double
   if (rc) return rc;
   return variant == HHG_VAR_NODAL ? launch_gs_volume<1>(G, S(stream))
                                   : launch_gs_volume<0>(G, S(stream));
+}
+
+// skewed (hyperplane-major) volume sweep: u and f gathered into the
+// hyperplane order, the sweep, u scattered back (hhg_smooth.cuh)
+static GSDesc gs_grid_desc(const hhg_grid *g, int variant, const double *coef, double omega,
+                           double *u, const double *f) {
+  GSDesc G{};
+  G.n = g->n;
+  G.ntets = g->ntets;
+  G.L = g->lat_size;
+  G.S = g->shell_size;
+  G.nvol = g->nvol;
+  G.vol_start = reinterpret_cast<const long long *>(g->vol_start);
+  G.srow = g->srow;
+  G.ghost = g->ghost;
+  G.kc = g->kc;
+  G.u = u;
+  G.f = f;
+  G.coef = coef;
+  G.coef_stride = variant == HHG_VAR_NODAL ? 72 : 14;
+  G.omega = omega;
+  G.lattice = 0;
+  return G;
+}
+
+int hhg_skew_coefficient(const hhg_grid *g, double *ks, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;
+  if (g->n < 4 || g->nvol == 0) return HHG_OK;
+  GSDesc G = gs_grid_desc(g, HHG_VAR_SCALING, nullptr, 1.0, nullptr, nullptr);
+  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code);
+  if (rc) return rc;
+  skew_move_kernel<2><<<dim3((int)((g->nvol + 255) / 256), g->ntets), 256, 0, S(stream)>>>(
+      G, nullptr, ks);
+  return check("skew_move_kernel");
+}
+
+int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef, double omega,
+                           double *u, const double *f, double *us, double *fs,
+                           const double *ks, void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;
+  if (g->n < 4 || g->nvol == 0) return HHG_OK;
+  if (!us || !fs || !ks) return HHG_ERR_ARG;
+  GSDesc G = gs_grid_desc(g, variant, coef, omega, u, f);
+  const int *start = nullptr;
+  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code, &start);
+  if (rc) return rc;
+  const dim3 mv((int)((g->nvol + 255) / 256), g->ntets);
+  skew_move_kernel<0><<<mv, 256, 0, S(stream)>>>(G, u, us);
+  if ((rc = check("skew_move_kernel"))) return rc;
+  skew_move_kernel<0><<<mv, 256, 0, S(stream)>>>(G, f, fs);
+  if ((rc = check("skew_move_kernel"))) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G.ntets * HHG_GS_CLUSTER);
+  cfg.stream = S(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = HHG_GS_CLUSTER;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cudaError_t e;
+  if (variant == HHG_VAR_NODAL) {
+    cfg.blockDim = dim3(gs_cluster_threads<1>());
+    e = cudaLaunchKernelEx(&cfg, gs_volume_skew_kernel<1>, G, (const double *)us, fs, ks, start);
+  } else {
+    cfg.blockDim = dim3(gs_cluster_threads<0>());
+    e = cudaLaunchKernelEx(&cfg, gs_volume_skew_kernel<0>, G, (const double *)us, fs, ks, start);
+  }
+  if (e != cudaSuccess) {
+    fprintf(stderr, "hhg_b200: gs_volume_skew_kernel: %s\n", cudaGetErrorString(e));
+    return HHG_ERR_CUDA;
+  }
+  skew_move_kernel<1><<<mv, 256, 0, S(stream)>>>(G, us, u);
+  return check("skew_move_kernel");
 }
 
 // ---------------------------------------------------------------------------

@@ -337,6 +337,110 @@ gs_volume_cluster_kernel(GSDesc D) {
   }
 }
 
+// Skewed (hyperplane-major) form of the volume sweep.  The interior points
+// of each element are stored in hyperplane order - h = i + 2j + 3k, then k,
+// then j - so one hyperplane is a contiguous run and the neighbours of
+// consecutive points of a run are consecutive points of the neighbouring
+// runs (direction d moves h by di + 2dj + 3dk): every load and store of the
+// sweep is coalesced.  u and f are gathered into this order before the
+// sweep and u scattered back after it (skew_move_kernel); k is gathered once
+// per operator (static).  Same points per hyperplane, same arithmetic as
+// gs_volume_kernel: bitwise the lexicographic sweep.
+//   MODE 0: dst[t nvol + e] = src[vol_start[t] + vrank(e)]   (gather)
+//   MODE 1: dst[vol_start[t] + vrank(e)] = src[t nvol + e]   (scatter)
+//   MODE 2: dst[t nvol + e] = kc[t L + lattice(e)]          (coefficient)
+template <int MODE>
+__global__ void skew_move_kernel(GSDesc D, const double *__restrict__ src,
+                                 double *__restrict__ dst) {
+  const int t = blockIdx.y;
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e >= D.nvol) return;
+  const int n = D.n;
+  const int code = __ldg(D.hp_code + e);
+  const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+  const long long sk = (long long)t * D.nvol + e;
+  if (MODE == 2) {
+    dst[sk] = __ldg(D.kc + (long long)t * D.L + lbase32(n, k, j) + i);
+    return;
+  }
+  const long long g = D.vol_start[t] + lbase32(n - 4, k - 1, j - 1) + i - 1;
+  if (MODE == 0) dst[sk] = __ldg(src + g);
+  else dst[g] = src[sk];
+}
+
+template <int VAR>
+__global__ void __launch_bounds__(gs_cluster_threads<VAR>())
+gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ fs,
+                      const double *__restrict__ ks, const int *__restrict__ start) {
+  double *us = const_cast<double *>(us_c);
+  const int cpt = (int)cluster_nctas();
+  const int t = blockIdx.x / cpt;
+  const int part = (int)cluster_ctarank();
+  const int n = D.n;
+  __shared__ double sfac[72];
+  double coef[14];
+  if (VAR == 0) {
+#pragma unroll
+    for (int d = 0; d < 14; ++d) coef[d] = D.coef[(long long)t * D.coef_stride + d];
+  } else {
+    for (int e = threadIdx.x; e < 72; e += blockDim.x)
+      sfac[e] = D.coef[(long long)t * D.coef_stride + e];
+    __syncthreads();
+  }
+  const double omega = D.omega;
+  const int hmin = 6, hmax = 3 * n - 6;
+  const double *kt = D.kc + (long long)t * D.L;
+  const double *gt = D.ghost + (long long)t * D.S;
+  double *ue = us + (long long)t * D.nvol;
+  const double *fe = fs + (long long)t * D.nvol;
+  const double *ke = ks + (long long)t * D.nvol;
+  const int stride = cpt * blockDim.x;
+  const int first = part * blockDim.x + threadIdx.x;
+  for (int h = hmin; h <= hmax; ++h) {
+    const int ha = __ldg(D.hp_ptr + h - hmin), hb = __ldg(D.hp_ptr + h + 1 - hmin);
+    for (int e = ha + first; e < hb; e += stride) {
+      const int code = __ldg(D.hp_code + e);
+      const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+      const IncPlanes P = inc_planes(n, k);
+      double2 q[14];
+#pragma unroll
+      for (int d = 0; d < 14; ++d) {
+        const int di = c_dirs_h(d, 0), dj = c_dirs_h(d, 1), dk = c_dirs_h(d, 2);
+        const int qi = i + di, qj = j + dj, qk = k + dk;
+        const bool inner = qi >= 1 && qj >= 1 && qk >= 1 && qi + qj + qk <= n - 1;
+        if (inner) {
+          const int hq = h + di + 2 * dj + 3 * dk;
+          const int pos = __ldg(start + (hq - hmin) * (n + 1) + qk) + qj;
+          q[d] = make_double2(__ldcg(ue + pos), __ldg(ke + pos));
+        } else {
+          int off;
+          inc_voff(P, dk + 1, n, qi, qj, qk, off);
+          q[d] = make_double2(__ldg(gt + off), __ldg(kt + inc_koff(P, dk + 1, qi, qj)));
+        }
+      }
+      const double k0 = __ldg(ke + e);
+      double acc = 0.0, diag = 0.0;
+      if (VAR == 0) {
+#pragma unroll
+        for (int d = 0; d < 14; ++d) {
+          const double sd = dmul(dadd(k0, q[d].y), coef[d]);
+          acc = dadd(acc, dmul(sd, q[d].x));
+          diag = dsub(diag, sd);
+        }
+      } else {
+        double b[55];
+        nodal_buffer(k0, q, b);
+        nodal_gs_terms<0>(acc, diag, q, b, sfac);
+      }
+      if (diag == 0.0) atomicOr(&g_status, 1);
+      const double old = __ldcg(ue + e);
+      __stcg(ue + e, dadd(dmul(dsub(1.0, omega), old),
+                          ddiv(dmul(omega, dsub(__ldg(fe + e), acc)), diag)));
+    }
+    cluster_sync_all();
+  }
+}
+
 // --- surface rows, one level per launch -----------------------------------
 struct SurfGSDesc {
   SurfDesc s;

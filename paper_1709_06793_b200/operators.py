@@ -628,9 +628,19 @@ class Operator:
             else:
                 var, coef = _lib.VAR["scaling"], D["sh"]
 
+            ws = self._skew_workspace()
+
             def volume():
-                check(lib.hhg_smooth_volume(dg.ref, var, coef.data_ptr(), float(omega),
-                                            du.data_ptr(), df.data_ptr(), st), "smooth_volume")
+                if ws is None:
+                    check(lib.hhg_smooth_volume(dg.ref, var, coef.data_ptr(), float(omega),
+                                                du.data_ptr(), df.data_ptr(), st),
+                          "smooth_volume")
+                    return
+                us, fs, ks = ws
+                check(lib.hhg_smooth_volume_skew(dg.ref, var, coef.data_ptr(), float(omega),
+                                                 du.data_ptr(), df.data_ptr(), us.data_ptr(),
+                                                 fs.data_ptr(), ks.data_ptr(), st),
+                      "smooth_volume_skew")
         if check_diag:
             lib.hhg_status_reset()
         for _ in range(sweeps):
@@ -643,6 +653,26 @@ class Operator:
             D["torch"].cuda.current_stream().synchronize()
             check(lib.hhg_status(), "smooth")
         return du
+
+    def _skew_workspace(self):
+        """(us, fs, ks) of the hyperplane-major volume sweep
+        (hhg_smooth_volume_skew): u and f copies per sweep, the skewed
+        coefficient once per operator; None below level 7, where the plain
+        cluster sweep is faster than the two gathers and the scatter)."""
+        D = self._device()
+        if "skew" not in D:
+            gt = D["grid"].gt
+            nv = gt.ntets * gt.nvol
+            if gt.n < 128 or nv == 0:
+                D["skew"] = None
+            else:
+                torch = D["torch"]
+                buf = torch.empty(3 * nv, dtype=torch.float64, device="cuda")
+                us, fs, ks = buf[:nv], buf[nv:2 * nv], buf[2 * nv:]
+                check(lib.hhg_skew_coefficient(D["grid"].ref, ks.data_ptr(), self._stream()),
+                      "skew_coefficient")
+                D["skew"] = (us, fs, ks)
+        return D["skew"]
 
     def smooth(self, u, f, sweeps=1, omega=1.0):
         """Forward Gauss-Seidel in global node order, in place; returns u."""

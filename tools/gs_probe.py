@@ -59,7 +59,11 @@ rng = np.random.default_rng(0)
 u0 = torch.as_tensor(rng.uniform(-1, 1, grid.n_nodes), device="cuda")
 f = torch.as_tensor(rng.uniform(-1, 1, grid.n_nodes), device="cuda")
 ref = None
+nv = grid.nodes_per_volume * grid.macro.n_elements
+ws = None
 for var in variants:
+    skew = var.endswith(":skew")
+    var = var.replace(":skew", "")
     defs, tag = tag_of(var)
     so = ROOT / "tools" / "_so" / f"{tag}.so"
     h = ctypes.CDLL(str(so))
@@ -73,7 +77,19 @@ for var in variants:
     st = torch.cuda.current_stream().cuda_stream
     u = u0.clone()
     h.hhg_ghost_update(dg.ref, u.data_ptr(), st)
-    rc = h.hhg_smooth_volume(dg.ref, 0, sh.data_ptr(), 1.0, u.data_ptr(), f.data_ptr(), st)
+    if skew:
+        if ws is None:
+            ws = torch.empty(3 * nv, dtype=torch.float64, device="cuda")
+        h.hhg_skew_coefficient(dg.ref, ws[2 * nv:].data_ptr(), st)
+
+    def sweep():
+        if skew:
+            return h.hhg_smooth_volume_skew(dg.ref, 0, sh.data_ptr(), 1.0, u.data_ptr(),
+                                            f.data_ptr(), ws.data_ptr(), ws[nv:].data_ptr(),
+                                            ws[2 * nv:].data_ptr(), st)
+        return h.hhg_smooth_volume(dg.ref, 0, sh.data_ptr(), 1.0, u.data_ptr(), f.data_ptr(),
+                                   st)
+    rc = sweep()
     torch.cuda.synchronize()
     if rc:
         print(var, "rc", rc, flush=True)
@@ -82,12 +98,12 @@ for var in variants:
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(3):
-        h.hhg_smooth_volume(dg.ref, 0, sh.data_ptr(), 1.0, u.data_ptr(), f.data_ptr(), st)
+        sweep()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 3
     if ref is None:
         ref = res
-    print(f"{var:50s} volume GS sweep {ms:8.3f} ms  bitwise={bool(torch.equal(res, ref))}",
+    print(f"{var + (' skewed' if skew else ''):50s} volume GS sweep {ms:8.3f} ms  bitwise={bool(torch.equal(res, ref))}",
           flush=True)
     del dg

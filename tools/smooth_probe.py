@@ -42,7 +42,13 @@ e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
 e0.record()
 check(lib.hhg_smooth_surface_all(dg.ref, ds.ref, gs["ref"], 1.0, u.data_ptr(), f.data_ptr(), st))
 e1.record()
-check(lib.hhg_smooth_volume(dg.ref, 0, D["sh"].data_ptr(), 1.0, u.data_ptr(), f.data_ptr(), st))
+ws = op._skew_workspace()
+if ws is None:
+    check(lib.hhg_smooth_volume(dg.ref, 0, D["sh"].data_ptr(), 1.0, u.data_ptr(), f.data_ptr(),
+                                st))
+else:
+    check(lib.hhg_smooth_volume_skew(dg.ref, 0, D["sh"].data_ptr(), 1.0, u.data_ptr(),
+                                     f.data_ptr(), *(x.data_ptr() for x in ws), st))
 e2.record()
 torch.cuda.synchronize()
 out = op.apply_device(u)
