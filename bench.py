@@ -271,7 +271,7 @@ def run_own(args):
         if i:
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         del res
-    e2e = statistics.median(e2e_ms)
+    e2e = statistics.median(e2e_ms) if e2e_ms else float("nan")
     if dist:
         t = torch.tensor([e2e], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -316,9 +316,9 @@ def run_own(args):
                          "step": {"algorithmic_bytes": step_bytes,
                                   "achieved": round(step_bytes / (ms * 1e-3) / 1e9, 1),
                                   "frac": round(step_bytes / (ms * 1e-3) / 1e9 / hbm, 4)}},
-            "e2e": {"value": round(total_dofs / (e2e * 1e-3) / 1e9, 4), "unit": "GDoF/s",
-                    "ms_per_step": round(e2e, 2), "h2d_bytes_per_step": 8 * grid.n_nodes,
-                    "d2h_bytes_per_step": 8 * grid.n_nodes},
+            "e2e": ({"value": round(total_dofs / (e2e * 1e-3) / 1e9, 4), "unit": "GDoF/s",
+                     "ms_per_step": round(e2e, 2), "h2d_bytes_per_step": 8 * grid.n_nodes,
+                     "d2h_bytes_per_step": 8 * grid.n_nodes} if e2e_ms else None),
             "gpu_launches": int(launches),
             "per_rank": per_rank,
             "all_rows_gdofs": round(grid.n_nodes * world / (ms * 1e-3) / 1e9, 3),

@@ -104,6 +104,21 @@ int hhg_gs_scaling_3d(int64_t n, const int64_t *base, double *u,
                       const double *fv, const double *kc, const double *sh,
                       double omega, void *stream);
 
+/* replaces kernels.apply_scaling_2d(n, base, v, kc, kg, g, sh, out),
+ * kernels.py:750-782: 2-D scaled stencil on a triangle lattice (row j at
+ * base[j] = j (n+1) - j (j-1)/2), v, kc, kg float64[(n+1)(n+2)/2], sh (6)
+ * and out ((n-1)(n-2)/2 rows) device pointers; g: 6 HOST flags, the
+ * uniform-ellipticity (MA2) gray-edge selector - direction d averages the
+ * safeguarded coefficient kg instead of kc where g[d] != 0 */
+int hhg_apply_scaling_2d(int64_t n, const int64_t *base, const double *v,
+                         const double *kc, const double *kg, const uint8_t *g,
+                         const double *sh, double *out, void *stream);
+/* replaces kernels.gs_scaling_2d(n, base, u, fv, kc, kg, g, sh, omega),
+ * kernels.py:906-937 (wavefronts i + 2j, bitwise the sequential sweep) */
+int hhg_gs_scaling_2d(int64_t n, const int64_t *base, double *u, const double *fv,
+                      const double *kc, const double *kg, const uint8_t *g,
+                      const double *sh, double omega, void *stream);
+
 /* replaces kernels.gs_nodal_3d(...), kernels.py:553-600 (tables as above) */
 int hhg_gs_nodal_3d(int64_t n, const int64_t *base, double *u,
                     const double *fv, const double *kc, const int64_t *sched,

@@ -292,6 +292,58 @@ int oracle_gs_nodal_tensor_3d(int64_t n, const int64_t *base, double *u, const d
 }
 
 /* kernels.py:979-992 */
+/* 2-D scaling kernels with the MA2 gray-edge selector (kernels.py:750-782,
+ * 906-937): triangle lattice, base[j] row starts, interior rows j in
+ * [1, n-2], i in [1, n-1-j]; direction d (DIRS_2D, mesh.py:41-43) uses the
+ * safeguarded coefficient kg when g[d] != 0, else kc */
+static inline void neighbours_2d(const int64_t *base, int64_t j, int64_t i, int64_t nb[6]) {
+  const int64_t b = base[j], bju = base[j + 1], bjd = base[j - 1], p = b + i;
+  nb[0] = p + 1;         nb[1] = bju + i;  nb[2] = bjd + i + 1;
+  nb[3] = p - 1;         nb[4] = bjd + i;  nb[5] = bju + i - 1;
+}
+
+void oracle_apply_scaling_2d(int64_t n, const int64_t *base, const double *v,
+                             const double *kc, const double *kg, const uint8_t *g,
+                             const double *sh, double *out) {
+  int64_t c = 0, nb[6];
+  for (int64_t j = 1; j < n - 1; ++j)
+    for (int64_t i = 1; i < n - j; ++i) {
+      const int64_t p = base[j] + i;
+      neighbours_2d(base, j, i, nb);
+      const double v0 = v[p];
+      double sd = g[0] ? (kg[p] + kg[p + 1]) * sh[0] : (kc[p] + kc[p + 1]) * sh[0];
+      double acc = sd * (v[p + 1] - v0);
+      for (int d = 1; d < 6; ++d) {
+        const int64_t q = nb[d];
+        sd = g[d] ? (kg[p] + kg[q]) * sh[d] : (kc[p] + kc[q]) * sh[d];
+        acc += sd * (v[q] - v0);
+      }
+      out[c++] = acc;
+    }
+}
+
+int oracle_gs_scaling_2d(int64_t n, const int64_t *base, double *u, const double *fv,
+                         const double *kc, const double *kg, const uint8_t *g,
+                         const double *sh, double omega) {
+  int64_t c = 0, nb[6];
+  for (int64_t j = 1; j < n - 1; ++j)
+    for (int64_t i = 1; i < n - j; ++i) {
+      const int64_t p = base[j] + i;
+      neighbours_2d(base, j, i, nb);
+      double acc = 0.0, diag = 0.0;
+      for (int d = 0; d < 6; ++d) {
+        const int64_t q = nb[d];
+        const double sd = g[d] ? (kg[p] + kg[q]) * sh[d] : (kc[p] + kc[q]) * sh[d];
+        acc += sd * u[q];
+        diag -= sd;
+      }
+      if (diag == 0.0) return ORACLE_ZERO_DIAG;
+      u[p] = (1.0 - omega) * u[p] + omega * (fv[c] - acc) / diag;
+      ++c;
+    }
+  return ORACLE_OK;
+}
+
 int oracle_csr_gs(int64_t nrows, const int64_t *rows, const int32_t *indptr,
                   const int32_t *indices, const double *data, const double *diag,
                   double *u, const double *f, double omega) {

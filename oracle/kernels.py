@@ -34,6 +34,8 @@ def _load():
         "oracle_csr_gs": (ctypes.c_int, [_I, _P, _P, _P, _P, _P, _P, _P, _D]),
         "oracle_apply_scaling_3d_batch": (None, [_I, _P, _I, _P, _P, _P, _P, _I]),
         "oracle_num_threads": (ctypes.c_int, []),
+        "oracle_apply_scaling_2d": (None, [_I, _P, _P, _P, _P, _P, _P, _P]),
+        "oracle_gs_scaling_2d": (ctypes.c_int, [_I, _P, _P, _P, _P, _P, _P, _P, _D]),
         "oracle_apply_scaling_tensor_3d": (None, [_I, _P, _P, _P, _I, _P, _P]),
         "oracle_apply_nodal_tensor_3d": (ctypes.c_int, [_I, _P, _P, _P, _I, _P, _I, _P, _P,
                                                         _P, _P, _P]),
@@ -167,6 +169,26 @@ def csr_gs(rows, indptr, indices, data, diag, u, f, omega):
          _c(data, float), _c(diag, float), _c(f, float)]
     rc = lib().oracle_csr_gs(len(a[0]), _p(a[0]), _p(a[1]), _p(a[2]), _p(a[3]),
                              _p(a[4]), _p(u), _p(a[5]), float(omega))
+    if rc:
+        raise ValueError("zero central stencil entry")
+    return u
+
+
+def apply_scaling_2d(n, base, v, kc, kg, g, sh):
+    """kernels.apply_scaling_2d with the MA2 gray-edge selector g (6 flags)."""
+    a = [_c(base, np.int64), _c(v, np.float64), _c(kc, np.float64), _c(kg, np.float64),
+         _c(np.asarray(g) != 0, np.uint8), _c(sh, np.float64)]
+    out = np.empty((n - 1) * (n - 2) // 2 if n >= 3 else 0)
+    lib().oracle_apply_scaling_2d(n, *(_p(x) for x in a), _p(out))
+    return out
+
+
+def gs_scaling_2d(n, base, u, fv, kc, kg, g, sh, omega):
+    """kernels.gs_scaling_2d, in place on u (float64, contiguous)."""
+    a = [_c(fv, np.float64), _c(kc, np.float64), _c(kg, np.float64),
+         _c(np.asarray(g) != 0, np.uint8), _c(sh, np.float64)]
+    rc = lib().oracle_gs_scaling_2d(n, _p(_c(base, np.int64)), _p(u), *(_p(x) for x in a),
+                                    omega)
     if rc:
         raise ValueError("zero central stencil entry")
     return u

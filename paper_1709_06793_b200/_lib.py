@@ -87,6 +87,9 @@ EXPORTS = {
     "hhg_apply_const_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp,
                                           ctypes.c_double, vp, vp]),
     "hhg_apply_stored_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp]),
+    "hhg_apply_scaling_2d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "hhg_gs_scaling_2d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp,
+                                         ctypes.c_double, vp]),
     "hhg_csr_gs": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp, vp, vp,
                                   ctypes.c_double, vp]),
     "hhg_gs_scaling_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, vp,

@@ -16,6 +16,7 @@
 #include "../../include/hhg_b200.h"
 #include "hhg_common.cuh"
 #include "hhg_smooth.cuh"
+#include "hhg_ma2.cuh"
 #include "hhg_surface.cuh"
 #include "hhg_surface_face.cuh"
 #include "hhg_tensor.cuh"
@@ -544,6 +545,35 @@ int hhg_csr_gs(int64_t nrows_list, const int64_t *rows, const int64_t *indptr,
       reinterpret_cast<const long long *>(indptr), reinterpret_cast<const long long *>(indices),
       data, diag, u, f, omega);
   return check("csr_gs_kernel");
+}
+
+// 2-D scaling with the MA2 gray-edge selector (hhg_ma2.cuh); gray: 6 host
+// flags (the reference's g), base: the canonical row table (or NULL)
+static unsigned gray_bits(const uint8_t *g) {
+  unsigned b = 0;
+  for (int d = 0; d < 6; ++d)
+    if (g && g[d]) b |= 1u << d;
+  return b;
+}
+
+int hhg_apply_scaling_2d(int64_t n, const int64_t *, const double *v, const double *kc,
+                         const double *kg, const uint8_t *g, const double *sh, double *out,
+                         void *stream) {
+  if (n > 1 << 15) return HHG_ERR_ARG;
+  if (n < 3) return HHG_OK;
+  const dim3 grid((unsigned)((n - 3 + 127) / 128), (unsigned)(n - 2));
+  apply_scaling_2d_kernel<<<grid, 128, 0, S(stream)>>>((int)n, v, kc, kg, gray_bits(g), sh, out);
+  return check("apply_scaling_2d_kernel");
+}
+
+int hhg_gs_scaling_2d(int64_t n, const int64_t *, double *u, const double *fv, const double *kc,
+                      const double *kg, const uint8_t *g, const double *sh, double omega,
+                      void *stream) {
+  if (n > 1 << 15) return HHG_ERR_ARG;
+  if (n < 3) return HHG_OK;
+  gs_scaling_2d_kernel<<<1, 256, 0, S(stream)>>>((int)n, u, fv, kc, kg, gray_bits(g), sh,
+                                                 omega);
+  return check("gs_scaling_2d_kernel");
 }
 
 int hhg_gs_scaling_3d(int64_t n, const int64_t *, double *u, const double *fv,

@@ -245,6 +245,37 @@ def sec_norms():
     save("norms", **out)
 
 
+def sec_ma2_2d():
+    """The reference's 2-D scaling kernels with the MA2 gray-edge selector
+    (kernels.apply_scaling_2d / gs_scaling_2d): directions with g[d] set use
+    the safeguarded coefficient kg instead of kc; seeded lattices, every
+    gray pair."""
+    out = {}
+    rng = np.random.default_rng(22)
+    for n in (8, 16):
+        lat = RM.SimplexLattice(2, n)
+        v = rng.uniform(-1, 1, lat.size)
+        kc = rng.uniform(0.5, 3.0, lat.size)
+        kg = rng.uniform(0.1, 1.0, lat.size)
+        fv = rng.uniform(-1, 1, (n - 1) * (n - 2) // 2)
+        h = rng.uniform(-1.0, 0.2, 3)
+        sh = np.concatenate([h, h])
+        out[f"n{n}_v"], out[f"n{n}_kc"], out[f"n{n}_kg"] = v, kc, kg
+        out[f"n{n}_fv"], out[f"n{n}_sh"] = fv, sh
+        for gp in (-1, 0, 1, 2):
+            g = np.zeros(6, dtype=np.bool_)
+            if gp >= 0:
+                g[gp] = g[gp + 3] = True
+            o = np.empty((n - 1) * (n - 2) // 2)
+            kn.apply_scaling_2d(n, lat.base, v, kc, kg, g, sh, o)
+            out[f"n{n}_g{gp}_apply"] = o
+            for om in (1.0, 0.8):
+                u = v.copy()
+                kn.gs_scaling_2d(n, lat.base, u, fv, kc, kg, g, sh, om)
+                out[f"n{n}_g{gp}_gs{int(om * 10)}"] = u
+    save("ma2_2d", **out)
+
+
 def sec_mg_small():
     """Multigrid V-cycles on small grids (fast pins of the solver loop)."""
     from hhgscale.coefficients import catalog
@@ -391,7 +422,7 @@ def sec_coeff():
 
 SECTIONS = {"mesh": sec_mesh, "kernels": sec_kernels, "applies": sec_applies,
             "c3": sec_c3_checksums, "c2": sec_c2_cg, "mg": sec_mg_small, "c4": sec_c4_mg,
-            "tensor": sec_tensor, "coeff": sec_coeff, "norms": sec_norms}
+            "tensor": sec_tensor, "coeff": sec_coeff, "norms": sec_norms, "ma2_2d": sec_ma2_2d}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(SECTIONS)):

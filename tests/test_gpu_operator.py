@@ -607,3 +607,29 @@ def test_no_writes_outside_the_output(cuda, cfg, variant, kw):
     torch.cuda.synchronize()
     assert torch.isnan(ubuf[:pad]).all() and torch.isnan(ubuf[pad + n:]).all()
     assert not torch.isnan(uu).any()
+
+
+def test_ma2_2d_kernels_bitwise(cuda):
+    """The 2-D scaling kernels with the MA2 gray-edge selector
+    (kernels.apply_scaling_2d / gs_scaling_2d) through the C ABI, against
+    the reference's own outputs, for every gray pair."""
+    torch = cuda
+    g = golden("ma2_2d")
+    st = torch.cuda.current_stream().cuda_stream
+    for n in (8, 16):
+        p = lambda k: g[f"n{n}_{k}"]
+        v, kc, kg, sh, fv = (_dev(torch, p(k)) for k in ("v", "kc", "kg", "sh", "fv"))
+        out = torch.empty((n - 1) * (n - 2) // 2, dtype=torch.float64, device="cuda")
+        for gp in (-1, 0, 1, 2):
+            sel = np.zeros(6, dtype=np.uint8)
+            if gp >= 0:
+                sel[gp] = sel[gp + 3] = 1
+            check(lib.hhg_apply_scaling_2d(n, None, v.data_ptr(), kc.data_ptr(), kg.data_ptr(),
+                                           sel.ctypes.data, sh.data_ptr(), out.data_ptr(), st))
+            assert np.array_equal(out.cpu().numpy(), p(f"g{gp}_apply")), (n, gp)
+            for om in (1.0, 0.8):
+                u = _dev(torch, p("v").copy())
+                check(lib.hhg_gs_scaling_2d(n, None, u.data_ptr(), fv.data_ptr(), kc.data_ptr(),
+                                            kg.data_ptr(), sel.ctypes.data, sh.data_ptr(), om,
+                                            st))
+                assert np.array_equal(u.cpu().numpy(), p(f"g{gp}_gs{int(om * 10)}")), (n, gp)

@@ -140,3 +140,22 @@ def test_assembled_oracle_structure():
         assert np.abs(s).max() < 1e-12 * scale                     # zero row sums
         R = assemble_global(grid, v, kf, reduced=True)
         assert abs(R - R.T).max() < 1e-12 * scale                  # symmetry
+
+
+def test_c_ma2_2d_kernels_bitwise():
+    """C restatement of the reference's 2-D scaling kernels with the MA2
+    gray-edge selector against the reference's own outputs."""
+    g = golden("ma2_2d")
+    for n in (8, 16):
+        base = np.array([j * (n + 1) - j * (j - 1) // 2 for j in range(n + 1)], dtype=np.int64)
+        p = lambda k: g[f"n{n}_{k}"]
+        for gp in (-1, 0, 1, 2):
+            sel = np.zeros(6, dtype=bool)
+            if gp >= 0:
+                sel[gp] = sel[gp + 3] = True
+            out = ok.apply_scaling_2d(n, base, p("v"), p("kc"), p("kg"), sel, p("sh"))
+            assert np.array_equal(out, p(f"g{gp}_apply")), (n, gp)
+            for om in (1.0, 0.8):
+                u = p("v").copy()
+                ok.gs_scaling_2d(n, base, u, p("fv"), p("kc"), p("kg"), sel, p("sh"), om)
+                assert np.array_equal(u, p(f"g{gp}_gs{int(om * 10)}")), (n, gp, om)
