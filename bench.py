@@ -280,10 +280,10 @@ def run_own(args):
     traffic = None
     tp = ROOT / "profiles" / "volume_traffic.json"
     if tp.exists():
-        tj = json.loads(tp.read_text())
-        if tj.get("level") == args.level and tj.get("ntets") == ntets and \
-                tj.get("arithmetic") == ("fma" if args.fast else "bitwise"):
-            traffic = tj.get("dram_bytes_per_launch")
+        for tj in json.loads(tp.read_text()).get("entries", []):
+            if tj.get("level") == args.level and tj.get("ntets") == ntets and \
+                    tj.get("arithmetic") == ("fma" if args.fast else "bitwise"):
+                traffic = tj.get("dram_bytes_per_launch")
 
     cpu = None
     if rank == 0 and world == 1:

@@ -8,6 +8,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import numpy as np
+
 __all__ = ["OpCount", "Traffic", "analytic_count", "traffic",
            "volume_apply_bytes", "operations_table"]
 
@@ -81,17 +83,31 @@ def apply_step_bytes(grid, op) -> int:
     """Bytes one full device-resident Operator.apply moves with this
     implementation's data structures (bench.py's step-level roofline): the
     volume kernel (volume_apply_bytes), the ghost-layer update (gather list
-    8 B + u 8 B + ghost write 8 B per shell point), the precomputed surface
-    rows (per entry a 4-B column, an 8-B weight and the 8-B neighbour value;
-    per row its 8-B offset, 8-B id, centre value and result) and the
-    Dirichlet identity rows (8-B id, read, write)."""
+    8 B + u 8 B + ghost write 8 B per shell point), the surface rows and
+    the Dirichlet identity rows (8-B id, read, write).  Surface rows:
+    face-tiled mode - per face point and layer (the face, and each incident
+    element's layer next to it) the static coefficient 8 B + id 4 B + u 8 B,
+    and the 8-B result; rows left to the precomputed rows (macro edges and
+    vertices, or all rows in "csr" mode) - per entry a 4-B column, an 8-B
+    weight and the 8-B neighbour value, per row its offset, id, centre
+    value and result (32 B)."""
     D = op._device()
     gt = D["grid"].gt
-    st = D["surf"].st
-    nent = int(st.entry_ptr()[-1])
-    nrows = len(st.rows)
+    ds = D["surf"]
+    st = ds.st
+    ptr = st.entry_ptr()
     vol = volume_apply_bytes(grid.level, gt.ntets)
     ghost = 24 * gt.ntets * gt.S
-    surf = 20 * nent + 32 * nrows
+    faces = getattr(ds, "faces", None)
+    if faces is not None and len(faces.faces) and ds.desc.nfaces:
+        npf = grid.nodes_per_face
+        surf = 0
+        for rec in faces.faces:
+            layers = 3 if rec[0][1] >= 0 else 2
+            surf += npf * (layers * 20 + 8)
+        sub = np.asarray(faces.sub_rows, dtype=np.int64)
+        surf += int(20 * (ptr[sub + 1] - ptr[sub]).sum() + 32 * len(sub))
+    else:
+        surf = 20 * int(ptr[-1]) + 32 * len(st.rows)
     dirich = 24 * len(st.dir_ids)
     return int(vol + ghost + surf + dirich)
