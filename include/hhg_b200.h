@@ -215,6 +215,13 @@ typedef struct hhg_surface {
   int32_t pad_;
 } hhg_surface;
 
+/* stencil dumps of all macro elements (kernels.dump_scaling_3d /
+ * dump_nodal_3d, kernels.py:293-376): w[t][c][15] = (centre, s_0..s_13)
+ * of volume row c; variant HHG_VAR_SCALING (coef: sh[14] per element) or
+ * HHG_VAR_NODAL (coef: fac[72]); the stored-stencil baseline's input */
+int hhg_dump_stencils(const hhg_grid *g, int variant, const double *coef, double *w,
+                      void *stream);
+
 /* refresh the ghost layers: ghost[e] = u[shell_gid[e]] */
 int hhg_ghost_update(const hhg_grid *g, const double *u, void *stream);
 

@@ -97,6 +97,7 @@ EXPORTS = {
     "hhg_gs_nodal_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp, c_i64p,
                                        ctypes.c_int64, c_i64p, vp, c_i64p, c_i64p,
                                        ctypes.c_double, vp]),
+    "hhg_dump_stencils": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int, vp, vp, vp]),
     "hhg_ghost_update": (ctypes.c_int, [ctypes.POINTER(HhgGrid), vp, vp]),
     "hhg_volume_apply": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int,
                                         ctypes.c_int, vp, vp, vp, vp, vp, vp]),

@@ -613,6 +613,21 @@ static VolDesc grid_desc(const hhg_grid *g) {
   return D;
 }
 
+int hhg_dump_stencils(const hhg_grid *g, int variant, const double *coef, double *w,
+                      void *stream) {
+  if (g->n > HHG_MAX_N) return HHG_ERR_ARG;
+  if (g->n < 4 || g->ntets == 0) return HHG_OK;
+  if (variant != HHG_VAR_SCALING && variant != HHG_VAR_NODAL) return HHG_ERR_ARG;
+  const dim3 grid(g->n - 3, g->ntets);
+  if (variant == HHG_VAR_NODAL)
+    dump_stencils_kernel<1><<<grid, 128, 0, S(stream)>>>(g->n, g->lat_size, g->nvol, g->kc,
+                                                         coef, 72, w);
+  else
+    dump_stencils_kernel<0><<<grid, 128, 0, S(stream)>>>(g->n, g->lat_size, g->nvol, g->kc,
+                                                         coef, 14, w);
+  return check("dump_stencils_kernel");
+}
+
 int hhg_ghost_update(const hhg_grid *g, const double *u, void *stream) {
   if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   const long long total = (long long)g->ntets * g->shell_size;

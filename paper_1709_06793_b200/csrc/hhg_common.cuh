@@ -194,6 +194,18 @@ __device__ __forceinline__ double nodal_row_exact(double v0, double k0,
   return nodal_acc<0>(0.0, v0, q, b, fac);
 }
 
+// dump form (kernels.py:330-376): row[1 + d] = s_d, tot += s_d
+template <int D, class FAC>
+__device__ __forceinline__ void dump_nodal_terms(double &tot, double *row, const double (&b)[55],
+                                                 const FAC &fac) {
+  if constexpr (D < 14) {
+    const double s = dir_sum<D>(b, fac);
+    row[1 + D] = s;
+    tot = dadd(tot, s);
+    dump_nodal_terms<D + 1>(tot, row, b, fac);
+  }
+}
+
 // GS form (kernels.py:553-600): acc += s_d u_d, diag -= s_d
 template <int D, class FAC>
 __device__ __forceinline__ void nodal_gs_terms(double &acc, double &diag,

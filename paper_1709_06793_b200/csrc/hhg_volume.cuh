@@ -321,6 +321,63 @@ __device__ __forceinline__ void scaling_rows_mirror(const Win<B> &lo, const Win<
   }
 }
 
+// Stencil dumps (kernels.dump_scaling_3d / dump_nodal_3d, kernels.py:293-376):
+// per volume row (k, j, i order) the 15 weights (centre, s_0 .. s_13) of all
+// macro elements, w[t][c][15] on the device - the stored-stencil baseline's
+// input (Operator.store_stencils).  Scaling: s_d = (k0 + k_q) sh_d; nodal:
+// the direction sums of the 40-add schedule; centre = -(s_0 + ... + s_13)
+// accumulated from 0 in d order, as the reference.  Grid (planes, elements).
+template <int VAR>
+__global__ void dump_stencils_kernel(int n, long long L, long long nvol, const double *kc,
+                                     const double *coef, int coef_stride, double *w) {
+  const int t = blockIdx.y, k = 1 + blockIdx.x;
+  if (k > n - 3) return;
+  __shared__ double sfac[72];
+  double sh[14];
+  const double *cf = coef + (long long)t * coef_stride;
+  if (VAR == 1) {
+    for (int e = threadIdx.x; e < 72; e += blockDim.x) sfac[e] = cf[e];
+    __syncthreads();
+  } else {
+#pragma unroll
+    for (int d = 0; d < 14; ++d) sh[d] = cf[d];
+  }
+  const double *kt = kc + (long long)t * L;
+  double *wt = w + (long long)t * nvol * 15;
+  const int m4 = n - 4;
+  const long long plane = tetra32(m4) - tetra32(m4 - (k - 1));   // first row of plane k
+  int off = 0;
+  for (int j = 1; j <= n - 2 - k; ++j) {
+    const int len = n - 1 - j - k;
+    for (int i0 = threadIdx.x; i0 < len; i0 += blockDim.x) {
+      const int i = 1 + i0;
+      double2 q[14];
+      const double k0 = kt[lbase32(n, k, j) + i];
+#pragma unroll
+      for (int d = 0; d < 14; ++d)
+        q[d].y = kt[lbase32(n, k + c_dirs_h(d, 2), j + c_dirs_h(d, 1)) + i + c_dirs_h(d, 0)];
+      double *row = wt + (plane + off + i0) * 15;
+      double tot = 0.0;
+      if (VAR == 0) {
+#pragma unroll
+        for (int d = 0; d < 14; ++d) {
+          const double sd = dmul(dadd(k0, q[d].y), sh[d]);
+          row[1 + d] = sd;
+          tot = dadd(tot, sd);
+        }
+      } else {
+        double b[55];
+#pragma unroll
+        for (int d = 0; d < 14; ++d) q[d].x = 0.0;
+        nodal_buffer(k0, q, b);
+        dump_nodal_terms<0>(tot, row, b, sfac);
+      }
+      row[0] = -tot;
+    }
+    off += len;
+  }
+}
+
 template <int VAR, bool FAST>
 struct RowOp;
 

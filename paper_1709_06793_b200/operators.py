@@ -57,6 +57,24 @@ def parse_hybrid_set(spec: str):
     return frozenset(out)
 
 
+class _StoredWeights:
+    """Device-resident stencil tables of a stored-variant operator:
+    [ntets * nvol * 15] on the GPU; item t is element t's (nvol, 15) table
+    copied to the host (numpy)."""
+
+    def __init__(self, dev, ntets, nvol):
+        self.device, self.ntets, self.nvol = dev, ntets, nvol
+
+    def __len__(self):
+        return self.ntets
+
+    def __getitem__(self, t):
+        if not 0 <= t < self.ntets:
+            raise IndexError(t)
+        a = t * self.nvol * 15
+        return self.device[a:a + self.nvol * 15].reshape(self.nvol, 15).cpu().numpy()
+
+
 class Operator:
     """One operator variant bound to a grid and coefficient, on the GPU."""
 
@@ -219,8 +237,7 @@ class Operator:
             coef = torch.as_tensor(self._coef, device="cuda").reshape(-1)
             w = None
             if self._stored is not None:
-                w = torch.as_tensor(np.ascontiguousarray(np.stack(self._stored)),
-                                    device="cuda").reshape(-1)
+                w = self._stored.device
             sh = torch.as_tensor(np.ascontiguousarray(np.stack(self._sh)) if self._sh
                                  else np.zeros((0, 14)), device="cuda").reshape(-1)
             fac = None
@@ -788,14 +805,34 @@ class Operator:
         return w
 
     def store_stencils(self):
-        """Precompute all volume stencils; returns the stored-variant twin."""
+        """Precompute all volume stencils; returns the stored-variant twin
+        (operators.py:549-561).  Scaling and nodal stencils are dumped on the
+        device by one kernel over all elements (hhg_dump_stencils, the
+        reference's dump kernels) and stay there; `_stored[t]` copies
+        element t's table to the host on demand."""
         op = object.__new__(Operator)
         op.__dict__.update(self.__dict__)
         op.variant = "stored"
         op.source_variant = self.variant
         op.flops_add = 0
         op.flops_mul = 0
-        op._stored = [self.stencil_weights(t) for t in range(self.grid.macro.n_elements)]
-        op.bytes_required = sum(w.nbytes for w in op._stored)
-        op._dev = None
+        ne, nv = self.grid.macro.n_elements, self._nvol
+        if self.is_tensor or self.variant == "const" or nv == 0:
+            w = np.stack([self.stencil_weights(t) for t in range(ne)]) if ne else \
+                np.zeros((0, nv, 15))
+            torch = require_cuda()
+            dev = torch.as_tensor(np.ascontiguousarray(w), device="cuda").reshape(-1)
+        else:
+            D = self._device()
+            torch = D["torch"]
+            dev = torch.empty(ne * nv * 15, dtype=torch.float64, device="cuda")
+            var = _lib.VAR["nodal"] if self.variant == "nodal" else _lib.VAR["scaling"]
+            coef = D["coef"] if self.variant == "nodal" else D["sh"]
+            check(lib.hhg_dump_stencils(D["grid"].ref, var, coef.data_ptr(), dev.data_ptr(),
+                                        self._stream()), "dump_stencils")
+        op._stored = _StoredWeights(dev, ne, nv)
+        op.bytes_required = ne * nv * 15 * 8
+        # the twin shares this operator's device grid / surface tables
+        op._dev = dict(self._device())
+        op._dev["w"] = dev
         return op

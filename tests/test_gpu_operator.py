@@ -633,3 +633,28 @@ def test_ma2_2d_kernels_bitwise(cuda):
                                             kg.data_ptr(), sel.ctypes.data, sh.data_ptr(), om,
                                             st))
                 assert np.array_equal(u.cpu().numpy(), p(f"g{gp}_gs{int(om * 10)}")), (n, gp)
+
+
+@pytest.mark.parametrize("variant", ["scaling", "nodal"])
+def test_device_stencil_dump_matches_host_restatement(cuda, variant):
+    """store_stencils dumps every element's (centre, s_0..s_13) table on the
+    device (hhg_dump_stencils); each equals the host restatement of the
+    reference's dump kernel bitwise, and the stored twin applies exactly
+    like the source operator's stencils."""
+    grid = M.RefinedGrid(case_mesh("c3"), 4)
+    kf = sample_nodal(k_c3(), grid)
+    op = Operator(grid, variant, kf)
+    st = op.store_stencils()
+    assert st.bytes_required == grid.macro.n_elements * grid.nodes_per_volume * 15 * 8
+    for t in (0, 17, 47):
+        assert np.array_equal(st.stencil_weights(t), op.stencil_weights(t)), t
+    u = np.random.default_rng(6).uniform(-1, 1, grid.n_nodes)
+    vol = _vol_mask(grid)
+    ref = np.empty(grid.nodes_per_volume * grid.macro.n_elements)
+    out = st.apply(u)
+    for t in range(grid.macro.n_elements):
+        w = op.stencil_weights(t)
+        uloc = u[grid.elem_gidx[t]]
+        want = ok.apply_stored_3d(grid.n, grid.lat.base, uloc, w)
+        s0 = grid.vol_start[t]
+        assert np.array_equal(out[s0:s0 + grid.nodes_per_volume], want), t
