@@ -453,6 +453,8 @@ int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr,
 
 /* rows of one volume tile (W*B) the kernels were compiled with */
 int hhg_volume_tile_rows(void);
+/* face tile of the face-tiled surface kernel: (a extent << 16) | b extent */
+int hhg_face_tile(void);
 /* columns of one tile of the mirror kernel (hhg_grid.mtiles) */
 int hhg_volume_tile_cols_mirror(void);
 

@@ -177,6 +177,7 @@ EXPORTS = {
     "hhg_build_info": (ctypes.c_char_p, []),
     "hhg_volume_tile_rows": (ctypes.c_int, []),
     "hhg_volume_tile_cols_mirror": (ctypes.c_int, []),
+    "hhg_face_tile": (ctypes.c_int, []),
     "hhg_host_gs_levels": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp]),
 }
 

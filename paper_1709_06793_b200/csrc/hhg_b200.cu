@@ -1258,7 +1258,8 @@ int hhg_status_reset(void) {
   return HHG_OK;
 }
 
-int hhg_volume_tile_rows(void) { return kW * kB; }   // W*B rows (W/4 warp rows of 4B)
+int hhg_volume_tile_rows(void) { return kW * kB; }
+int hhg_face_tile(void) { return FACE_TA << 16 | FACE_TB; }   // W*B rows (W/4 warp rows of 4B)
 int hhg_volume_tile_cols_mirror(void) { return 8 * HHG_MIRROR_NW; }
 
 // host-side level schedule of the surface Gauss-Seidel: rows are in

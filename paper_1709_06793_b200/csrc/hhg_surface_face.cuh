@@ -26,7 +26,10 @@
 
 namespace hhg {
 
-constexpr int FACE_TA = 32, FACE_TB = 8;   // face tile: 32 (a) x 8 (b) points
+#ifndef HHG_FACE_TB
+#define HHG_FACE_TB 8
+#endif
+constexpr int FACE_TA = 32, FACE_TB = HHG_FACE_TB;   // face tile: 32 (a) x TB (b) points
 constexpr int FACE_W = FACE_TA + 2, FACE_H = FACE_TB + 2;   // staged region (halo 1)
 
 template <bool RES, bool MIXED>

@@ -218,7 +218,6 @@ class SurfaceTables:
         return np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
 
 
-FACE_TA, FACE_TB = 32, 8     # face tile of surface_face_kernel (hhg_surface_face.cuh)
 
 
 def _face_layers(A, cls):
@@ -278,7 +277,12 @@ class FaceTables:
     every lattice point (k never changes, so the kernel gathers only u).
     The remaining surface rows (macro edges and vertices) form a sub-list."""
 
-    def __init__(self, grid, gt: GridTables, st: SurfaceTables, kc_values):
+    def __init__(self, grid, gt: GridTables, st: SurfaceTables, kc_values, tile=None):
+        if tile is None:
+            ft = int(lib.hhg_face_tile())
+            tile = (ft >> 16, ft & 0xffff)
+        ta, tb = tile
+        self.tile = tile
         n = grid.n
         m = grid.macro
         rows = np.asarray(st.rows)
@@ -339,8 +343,8 @@ class FaceTables:
             gs.append(gl)
             covered[r0:r0 + npf] = True
             fid = len(recs) - 1
-            for b0 in range(1, n - 1, FACE_TB):
-                for a0 in range(1, n - b0, FACE_TA):
+            for b0 in range(1, n - 1, tb):
+                for a0 in range(1, n - b0, ta):
                     tiles.append((fid, a0, b0, 0))
         self.faces = recs
         self.tiles = np.ascontiguousarray(np.array(tiles, dtype=np.int32).reshape(-1, 4))

@@ -315,13 +315,12 @@ class Operator:
                      push=None):
         """Device-resident A u (or f - A u when f is given), torch tensors.
 
-        Order: ghost update, volume rows, surface + Dirichlet rows.  With
+        Order: ghost update, then the volume rows and the surface + Dirichlet
+        rows.  The surface rows - disjoint from the volume rows - run right
+        after the ghost update on a side stream, followed by
         ``after_surface(out)`` (the sharded operator's interface exchange)
-        the surface rows - disjoint from the volume rows - run right after
-        the ghost update on a side stream followed by the callable,
-        concurrently with the volume kernel; the side stream joins before
-        returning.  (Running the surface rows concurrently also on one GPU
-        measured no gain: 2.208 vs 2.22 ms per apply at config 5.)
+        when given, concurrently with the volume kernel; the side stream
+        joins before returning.
         ``volume_events``: optional (start, end) CUDA events recorded around
         the volume kernel on the launching stream (bench.py)."""
         D = self._device()
@@ -334,7 +333,12 @@ class Operator:
         flags = self._vol_flags(residual=f is not None)
         res = flags & _lib.FLAG_RESIDUAL
         fp = f.data_ptr() if f is not None else None
-        concurrent = self.surface_mode != "matrix-free" and after_surface is not None
+        # surface rows on a side stream, concurrently with the volume kernel
+        # (always with an exchange hook; on one GPU from level 6 on, where
+        # the face-tiled rows overlap the latency-bound volume kernel:
+        # 1.938 -> 1.913 ms per config-5 apply, tools/overlap_probe.py)
+        concurrent = self.surface_mode != "matrix-free" and (
+            after_surface is not None or self.grid.n >= 64)
         # the surface rows read shell values from the ghost layer: refresh first
         check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
         if concurrent:
