@@ -447,9 +447,27 @@ int hhg_tensor_surface_prepare(const hhg_grid *g, const hhg_surface *s,
                                const hhg_surface_gs *gs, int M, const double *km,
                                void *stream);
 
-/* HOST helper: level schedule of the surface Gauss-Seidel (see .cu) */
+/* HOST helper: level schedule of the surface Gauss-Seidel (see .cu);
+ * _seeded: with lower bounds seed[r] (NULL = 0) */
 int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr,
                        const int64_t *dep_idx, int64_t *level);
+int hhg_host_gs_levels_seeded(int64_t nrows, const int64_t *dep_ptr,
+                              const int64_t *dep_idx, const int64_t *seed, int64_t *level);
+
+/* sharded surface sweep (one level of the global schedule, explicit row
+ * index lists): rows updated directly; the partial row sums of shared
+ * interface rows (acc over this rank's incidences, its part of the
+ * diagonal) and the update from the rank-ordered sums of both sides */
+int hhg_smooth_surface_rows(const hhg_grid *g, const hhg_surface *s,
+                            const hhg_surface_gs *gs, const int64_t *rows, int64_t count,
+                            double omega, double *u, const double *f, void *stream);
+int hhg_smooth_surface_partial(const hhg_grid *g, const hhg_surface *s,
+                               const hhg_surface_gs *gs, const int64_t *rows, int64_t count,
+                               const double *u, double *acc, double *diag, void *stream);
+int hhg_smooth_surface_finish(const hhg_grid *g, const hhg_surface *s,
+                              const hhg_surface_gs *gs, const int64_t *rows, int64_t count,
+                              const double *acc, const double *diag, double omega,
+                              double *u, const double *f, void *stream);
 
 /* rows of one volume tile (W*B) the kernels were compiled with */
 int hhg_volume_tile_rows(void);

@@ -179,6 +179,20 @@ EXPORTS = {
     "hhg_volume_tile_cols_mirror": (ctypes.c_int, []),
     "hhg_face_tile": (ctypes.c_int, []),
     "hhg_host_gs_levels": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp]),
+    "hhg_host_gs_levels_seeded": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp]),
+    "hhg_smooth_surface_rows": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                               ctypes.POINTER(HhgSurface),
+                                               ctypes.POINTER(HhgSurfaceGS), vp,
+                                               ctypes.c_int64, ctypes.c_double, vp, vp, vp]),
+    "hhg_smooth_surface_partial": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                                  ctypes.POINTER(HhgSurface),
+                                                  ctypes.POINTER(HhgSurfaceGS), vp,
+                                                  ctypes.c_int64, vp, vp, vp, vp]),
+    "hhg_smooth_surface_finish": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                                 ctypes.POINTER(HhgSurface),
+                                                 ctypes.POINTER(HhgSurfaceGS), vp,
+                                                 ctypes.c_int64, vp, vp, ctypes.c_double, vp,
+                                                 vp, vp]),
 }
 
 

@@ -871,6 +871,53 @@ static int surface_csr(const hhg_grid *g, const hhg_surface *s, const hhg_surfac
 
 extern "C" {
 
+// sharded surface sweep pieces (rows of one level of the global schedule)
+static SurfGSDesc surf_gs_desc(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
+                               double omega, double *u, const double *f) {
+  SurfGSDesc G{};
+  G.s = surf_desc(g, s);
+  G.s.u = u;
+  G.s.f = f;
+  G.shell_gid = reinterpret_cast<const long long *>(g->shell_gid);
+  G.omega = omega;
+  G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
+  G.ent_col = gs->ent_col;
+  G.ent_val = gs->ent_val;
+  G.row_diag = gs->row_diag;
+  return G;
+}
+
+int hhg_smooth_surface_rows(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
+                            const int64_t *rows, int64_t count, double omega, double *u,
+                            const double *f, void *stream) {
+  if (count <= 0) return HHG_OK;
+  SurfGSDesc G = surf_gs_desc(g, s, gs, omega, u, f);
+  gs_surface_rows_kernel<<<(int)((count + 127) / 128), 128, 0, S(stream)>>>(
+      G, reinterpret_cast<const long long *>(rows), count);
+  return check("gs_surface_rows_kernel");
+}
+
+int hhg_smooth_surface_partial(const hhg_grid *g, const hhg_surface *s,
+                               const hhg_surface_gs *gs, const int64_t *rows, int64_t count,
+                               const double *u, double *acc, double *diag, void *stream) {
+  if (count <= 0) return HHG_OK;
+  SurfGSDesc G = surf_gs_desc(g, s, gs, 1.0, const_cast<double *>(u), nullptr);
+  gs_surface_partial_kernel<<<(int)((count + 127) / 128), 128, 0, S(stream)>>>(
+      G, reinterpret_cast<const long long *>(rows), count, acc, diag);
+  return check("gs_surface_partial_kernel");
+}
+
+int hhg_smooth_surface_finish(const hhg_grid *g, const hhg_surface *s,
+                              const hhg_surface_gs *gs, const int64_t *rows, int64_t count,
+                              const double *acc, const double *diag, double omega, double *u,
+                              const double *f, void *stream) {
+  if (count <= 0) return HHG_OK;
+  SurfGSDesc G = surf_gs_desc(g, s, gs, omega, u, f);
+  gs_surface_finish_kernel<<<(int)((count + 127) / 128), 128, 0, S(stream)>>>(
+      G, reinterpret_cast<const long long *>(rows), count, acc, diag);
+  return check("gs_surface_finish_kernel");
+}
+
 // every level of the surface sweep in one cooperative launch; the grid is
 // sized to the mean level width (a narrow sweep syncs few blocks)
 int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
@@ -1268,9 +1315,16 @@ int hhg_volume_tile_cols_mirror(void) { return 8 * HHG_MIRROR_NW; }
 // in one ascending pass (O(nnz)).  Returns the number of levels.
 int hhg_host_gs_levels(int64_t nrows, const int64_t *dep_ptr, const int64_t *dep_idx,
                        int64_t *level) {
+  return hhg_host_gs_levels_seeded(nrows, dep_ptr, dep_idx, nullptr, level);
+}
+
+// the same with lower bounds seed[r] (sharded sweeps: the levels the
+// neighbour rank computed for the shared interface rows)
+int hhg_host_gs_levels_seeded(int64_t nrows, const int64_t *dep_ptr, const int64_t *dep_idx,
+                              const int64_t *seed, int64_t *level) {
   int64_t nlev = 0;
   for (int64_t r = 0; r < nrows; ++r) {
-    int64_t lv = 0;
+    int64_t lv = seed ? seed[r] : 0;
     for (int64_t e = dep_ptr[r]; e < dep_ptr[r + 1]; ++e) {
       const int64_t q = dep_idx[e];
       if (q >= r) return HHG_ERR_ARG;

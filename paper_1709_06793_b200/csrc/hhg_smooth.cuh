@@ -609,6 +609,43 @@ __device__ __forceinline__ void gs_surface_row_csr(const SurfGSDesc &G, long lon
   u[gid] = dadd(dmul(dsub(1.0, om), __ldcg(u + gid)), ddiv(dmul(om, dsub(D.f[gid], acc)), diag));
 }
 
+// Sharded surface sweep (shard_mg.py): the rows of one level of the global
+// schedule, as explicit lists.  Rows owned by this rank alone update
+// directly; a row on an interface plane is shared with the neighbour rank,
+// whose macro elements contribute the other part of its sum: each rank forms
+// its partial (acc over its own incidences, its part of the diagonal), the
+// partials are exchanged and added in rank order, and both ranks finish
+// the row with the same numbers.
+__global__ void gs_surface_rows_kernel(SurfGSDesc G, const long long *rows, long long count) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < count) gs_surface_row_csr(G, rows[e]);
+}
+
+__global__ void gs_surface_partial_kernel(SurfGSDesc G, const long long *rows, long long count,
+                                          double *acc, double *diag) {
+  const long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (x >= count) return;
+  const long long r = rows[x];
+  const double *u = G.s.u;
+  double a = 0.0;
+  for (long long e = G.ent_ptr[r]; e < G.ent_ptr[r + 1]; ++e)
+    a = dadd(a, dmul(__ldg(G.ent_val + e), __ldcg(u + (unsigned)__ldg(G.ent_col + e))));
+  acc[x] = a;
+  diag[x] = G.row_diag[r];
+}
+
+__global__ void gs_surface_finish_kernel(SurfGSDesc G, const long long *rows, long long count,
+                                         const double *acc, const double *diag) {
+  const long long x = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (x >= count) return;
+  const long long gid = G.s.rows[rows[x]];
+  double *u = const_cast<double *>(G.s.u);
+  const double d = diag[x];
+  if (d == 0.0) atomicOr(&g_status, 1);
+  const double om = G.omega;
+  u[gid] = dadd(dmul(dsub(1.0, om), __ldcg(u + gid)), ddiv(dmul(om, dsub(G.s.f[gid], acc[x])), d));
+}
+
 // apply / residual of the surface rows from the precomputed weights:
 // part = sum_d w_d (v_d - v0) per incidence (direction order), row = sum of
 // parts (incidence order) — the association of surface_partial_kernel +

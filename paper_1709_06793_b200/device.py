@@ -184,8 +184,10 @@ class SurfaceTables:
             out[ok, d] = grid.elem_gidx[self.inc_tet[ok], flat]
         return out
 
-    def gs_levels(self):
-        """Level schedule of the forward surface GS (ascending-id order)."""
+    def gs_dag(self):
+        """Dependencies of the forward surface GS (ascending-id order): row r
+        reads the new values of dep_idx[dep_ptr[r]:dep_ptr[r+1]] (its lower-
+        id neighbour rows).  Returns (dep_ptr, dep_idx) int64."""
         nb = self.neighbour_gids()
         rows = self.rows
         nrows = len(rows)
@@ -199,11 +201,26 @@ class SurfaceTables:
         pairs = np.unique(np.column_stack([src[m], dep_row[m]]), axis=0)
         dep_ptr = np.searchsorted(pairs[:, 0], np.arange(nrows + 1)).astype(np.int64)
         dep_idx = np.ascontiguousarray(pairs[:, 1], dtype=np.int64)
+        return dep_ptr, dep_idx
+
+    @staticmethod
+    def levels_of(dag, seed=None):
+        """level[r] = max(seed[r], 1 + max level of r's dependencies)."""
+        dep_ptr, dep_idx = dag
+        nrows = len(dep_ptr) - 1
         level = np.zeros(nrows, dtype=np.int64)
-        nlev = lib.hhg_host_gs_levels(
-            nrows, dep_ptr.ctypes.data, dep_idx.ctypes.data, level.ctypes.data)
+        sd = None if seed is None else np.ascontiguousarray(seed, dtype=np.int64)
+        nlev = lib.hhg_host_gs_levels_seeded(nrows, dep_ptr.ctypes.data, dep_idx.ctypes.data,
+                                             None if sd is None else sd.ctypes.data,
+                                             level.ctypes.data)
         if nlev < 0:
             raise AssertionError("surface dependency list is not lower triangular")
+        return level
+
+    def gs_levels(self):
+        """Level schedule of the forward surface GS (ascending-id order)."""
+        level = self.levels_of(self.gs_dag())
+        nlev = int(level.max()) + 1 if len(level) else 0
         order = np.argsort(level, kind="stable")
         level_ptr = np.searchsorted(level[order], np.arange(nlev + 1))
         return order.astype(np.int64), level_ptr.astype(np.int64), int(nlev)

@@ -611,22 +611,13 @@ class Operator:
         df, _ = self._to_dev(f, "right-hand side")
         return self._from_dev(self.apply_device(du, f=df), kind)
 
-    def smooth_device(self, du, df, sweeps=1, omega=1.0, check_diag=True):
-        """Forward GS on device tensors.  Surface rows level by level, ghost
-        refresh, then volume wavefronts.  const / stored smooth with the
-        scaling (or, for a nodal source, nodal) sweep: their stencil weights
-        are bitwise those rows ((c+c)*sh == (c*2)*sh; dumped weights are the
-        scaling/nodal row terms).
-
-        ``check_diag``: synchronise and raise the reference's "zero central
-        stencil entry" ValueError here (the public ``smooth``).  The
-        multigrid cycle passes False and checks the shared status word once
-        per solve, so a V-cycle enqueues its sweeps without host round
-        trips."""
+    def _volume_sweeper(self, du, df, omega):
+        """Callable running one volume Gauss-Seidel sweep of every element
+        (hyperplane wavefronts; reads the ghost layer, which must be current)
+        on device tensors du, df."""
         D = self._device()
-        dg, ds = D["grid"], D["surf"]
+        dg = D["grid"]
         st = self._stream()
-        gs = ds.gs_tables(dg)
         src = getattr(self, "source_variant", self.variant)
         if self.is_tensor:
             var = _lib.VAR["nodal"] if src == "nodal" else _lib.VAR["scaling"]
@@ -643,25 +634,42 @@ class Operator:
                                                    df.data_ptr(),
                                                    self._lattice_work().data_ptr(), st),
                       "tensor_smooth_volume")
+            return volume
+        if src == "nodal":
+            var, coef = _lib.VAR["nodal"], D["coef"] if self._stored is None else D["fac"]
         else:
-            if src == "nodal":
-                var, coef = _lib.VAR["nodal"], D["coef"] if self._stored is None else D["fac"]
-            else:
-                var, coef = _lib.VAR["scaling"], D["sh"]
+            var, coef = _lib.VAR["scaling"], D["sh"]
+        ws = self._skew_workspace()
 
-            ws = self._skew_workspace()
+        def volume():
+            if ws is None:
+                check(lib.hhg_smooth_volume(dg.ref, var, coef.data_ptr(), float(omega),
+                                            du.data_ptr(), df.data_ptr(), st), "smooth_volume")
+                return
+            us, fs, ks = ws
+            check(lib.hhg_smooth_volume_skew(dg.ref, var, coef.data_ptr(), float(omega),
+                                             du.data_ptr(), df.data_ptr(), us.data_ptr(),
+                                             fs.data_ptr(), ks.data_ptr(), st),
+                  "smooth_volume_skew")
+        return volume
 
-            def volume():
-                if ws is None:
-                    check(lib.hhg_smooth_volume(dg.ref, var, coef.data_ptr(), float(omega),
-                                                du.data_ptr(), df.data_ptr(), st),
-                          "smooth_volume")
-                    return
-                us, fs, ks = ws
-                check(lib.hhg_smooth_volume_skew(dg.ref, var, coef.data_ptr(), float(omega),
-                                                 du.data_ptr(), df.data_ptr(), us.data_ptr(),
-                                                 fs.data_ptr(), ks.data_ptr(), st),
-                      "smooth_volume_skew")
+    def smooth_device(self, du, df, sweeps=1, omega=1.0, check_diag=True):
+        """Forward GS on device tensors.  Surface rows level by level, ghost
+        refresh, then volume wavefronts.  const / stored smooth with the
+        scaling (or, for a nodal source, nodal) sweep: their stencil weights
+        are bitwise those rows ((c+c)*sh == (c*2)*sh; dumped weights are the
+        scaling/nodal row terms).
+
+        ``check_diag``: synchronise and raise the reference's "zero central
+        stencil entry" ValueError here (the public ``smooth``).  The
+        multigrid cycle passes False and checks the shared status word once
+        per solve, so a V-cycle enqueues its sweeps without host round
+        trips."""
+        D = self._device()
+        dg, ds = D["grid"], D["surf"]
+        st = self._stream()
+        gs = ds.gs_tables(dg)
+        volume = self._volume_sweeper(du, df, omega)
         if check_diag:
             lib.hhg_status_reset()
         for _ in range(sweeps):

@@ -89,12 +89,16 @@ def exchange_partials(out, imap: InterfaceMap, dist, index_tensors=None):
     import torch
     if not imap.neighbours:
         return out
+    # gloo moves host tensors only: stage device vectors through host memory
+    stage = out.is_cuda and dist.get_backend() == "gloo"
     ops, recv, ids_t = [], {}, {}
     for nbr, ids in imap.neighbours.items():
         idx = index_tensors[nbr] if index_tensors is not None else \
             torch.as_tensor(ids, device=out.device)
         ids_t[nbr] = idx
         send = out.index_select(0, idx).contiguous()
+        if stage:
+            send = send.cpu()
         buf = torch.empty_like(send)
         recv[nbr] = (send, buf)
         ops.append(dist.P2POp(dist.isend, send, nbr))
@@ -103,7 +107,7 @@ def exchange_partials(out, imap: InterfaceMap, dist, index_tensors=None):
         req.wait()
     for nbr, (mine, theirs) in recv.items():
         total = (theirs + mine) if nbr < imap.rank else (mine + theirs)
-        out.index_copy_(0, ids_t[nbr], total)
+        out.index_copy_(0, ids_t[nbr], total.to(out.device))
     return out
 
 
