@@ -368,6 +368,10 @@ __global__ void skew_move_kernel(GSDesc D, const double *__restrict__ src,
   else dst[g] = src[sk];
 }
 
+#ifndef HHG_GS_SKEW_P
+#define HHG_GS_SKEW_P 1          // points per thread with loads in flight together (2: slower, registers)
+#endif
+
 template <int VAR>
 __global__ void __launch_bounds__(gs_cluster_threads<VAR>())
 gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ fs,
@@ -396,46 +400,70 @@ gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ f
   const double *ke = ks + (long long)t * D.nvol;
   const int stride = cpt * blockDim.x;
   const int first = part * blockDim.x + threadIdx.x;
-  for (int h = hmin; h <= hmax; ++h) {
-    const int ha = __ldg(D.hp_ptr + h - hmin), hb = __ldg(D.hp_ptr + h + 1 - hmin);
-    for (int e = ha + first; e < hb; e += stride) {
-      const int code = __ldg(D.hp_code + e);
-      const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
-      const IncPlanes P = inc_planes(n, k);
-      double2 q[14];
+  // a point's loads (neighbour values and coefficients, own old value, f)
+  // and its update, split so that two points' loads are in flight together
+  struct Pt {
+    double2 q[14];
+    double k0, fv, old;
+  };
+  auto gather = [&](int h, int e, Pt &X) {
+    const int code = __ldg(D.hp_code + e);
+    const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+    const IncPlanes P = inc_planes(n, k);
+#pragma unroll
+    for (int d = 0; d < 14; ++d) {
+      const int di = c_dirs_h(d, 0), dj = c_dirs_h(d, 1), dk = c_dirs_h(d, 2);
+      const int qi = i + di, qj = j + dj, qk = k + dk;
+      const bool inner = qi >= 1 && qj >= 1 && qk >= 1 && qi + qj + qk <= n - 1;
+      if (inner) {
+        const int hq = h + di + 2 * dj + 3 * dk;
+        const int pos = __ldg(start + (hq - hmin) * (n + 1) + qk) + qj;
+        X.q[d] = make_double2(__ldcg(ue + pos), __ldg(ke + pos));
+      } else {
+        int off;
+        inc_voff(P, dk + 1, n, qi, qj, qk, off);
+        X.q[d] = make_double2(__ldg(gt + off), __ldg(kt + inc_koff(P, dk + 1, qi, qj)));
+      }
+    }
+    X.k0 = __ldg(ke + e);
+    X.fv = __ldg(fe + e);
+    X.old = __ldcg(ue + e);
+  };
+  auto finish = [&](int e, const Pt &X) {
+    double acc = 0.0, diag = 0.0;
+    if (VAR == 0) {
 #pragma unroll
       for (int d = 0; d < 14; ++d) {
-        const int di = c_dirs_h(d, 0), dj = c_dirs_h(d, 1), dk = c_dirs_h(d, 2);
-        const int qi = i + di, qj = j + dj, qk = k + dk;
-        const bool inner = qi >= 1 && qj >= 1 && qk >= 1 && qi + qj + qk <= n - 1;
-        if (inner) {
-          const int hq = h + di + 2 * dj + 3 * dk;
-          const int pos = __ldg(start + (hq - hmin) * (n + 1) + qk) + qj;
-          q[d] = make_double2(__ldcg(ue + pos), __ldg(ke + pos));
-        } else {
-          int off;
-          inc_voff(P, dk + 1, n, qi, qj, qk, off);
-          q[d] = make_double2(__ldg(gt + off), __ldg(kt + inc_koff(P, dk + 1, qi, qj)));
-        }
+        const double sd = dmul(dadd(X.k0, X.q[d].y), coef[d]);
+        acc = dadd(acc, dmul(sd, X.q[d].x));
+        diag = dsub(diag, sd);
       }
-      const double k0 = __ldg(ke + e);
-      double acc = 0.0, diag = 0.0;
-      if (VAR == 0) {
-#pragma unroll
-        for (int d = 0; d < 14; ++d) {
-          const double sd = dmul(dadd(k0, q[d].y), coef[d]);
-          acc = dadd(acc, dmul(sd, q[d].x));
-          diag = dsub(diag, sd);
-        }
+    } else {
+      double b[55];
+      nodal_buffer(X.k0, X.q, b);
+      nodal_gs_terms<0>(acc, diag, X.q, b, sfac);
+    }
+    if (diag == 0.0) atomicOr(&g_status, 1);
+    __stcg(ue + e, dadd(dmul(dsub(1.0, omega), X.old),
+                        ddiv(dmul(omega, dsub(X.fv, acc)), diag)));
+  };
+  for (int h = hmin; h <= hmax; ++h) {
+    const int ha = __ldg(D.hp_ptr + h - hmin), hb = __ldg(D.hp_ptr + h + 1 - hmin);
+    for (int e = ha + first; e < hb; e += HHG_GS_SKEW_P * stride) {
+      if constexpr (HHG_GS_SKEW_P >= 2 && VAR == 0) {
+        Pt a, b;
+        gather(h, e, a);
+        const bool two = e + stride < hb;
+        if (two) gather(h, e + stride, b);
+        finish(e, a);
+        if (two) finish(e + stride, b);
       } else {
-        double b[55];
-        nodal_buffer(k0, q, b);
-        nodal_gs_terms<0>(acc, diag, q, b, sfac);
+        for (int x = 0, ee = e; x < HHG_GS_SKEW_P && ee < hb; ++x, ee += stride) {
+          Pt a;
+          gather(h, ee, a);
+          finish(ee, a);
+        }
       }
-      if (diag == 0.0) atomicOr(&g_status, 1);
-      const double old = __ldcg(ue + e);
-      __stcg(ue + e, dadd(dmul(dsub(1.0, omega), old),
-                          ddiv(dmul(omega, dsub(__ldg(fe + e), acc)), diag)));
     }
     cluster_sync_all();
   }
