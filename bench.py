@@ -178,6 +178,11 @@ def run_own(args):
     t_setup = time.time()
     grid, kf, op, u, imap = build_workload(rank, world, args.level, args.nx, args.variant,
                                            args.fast)
+    # the CPU baseline runs before any GPU work of this process (after the
+    # GPU work the host measured up to 1.5x slower in round 1)
+    cpu = None
+    if rank == 0 and world == 1:
+        cpu = cpu_baseline(grid, kf, op, u, args.cpu_tets, reps=3)
     D = op._device()
     du = torch.as_tensor(u, device="cuda")
     out = torch.empty_like(du)
@@ -285,10 +290,6 @@ def run_own(args):
                     tj.get("arithmetic") == ("fma" if args.fast else "bitwise"):
                 traffic = tj.get("dram_bytes_per_launch")
 
-    cpu = None
-    if rank == 0 and world == 1:
-        cpu = cpu_baseline(grid, kf, op, u, args.cpu_tets, reps=3)
-
     if rank == 0:
         flags = op._vol_flags()
         arith = ("fma edge-flux, mirror edge reuse (<= 1e-12 of the reference order)"
@@ -378,6 +379,16 @@ def run_dry(args):
         dist.destroy_process_group()
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline(grid, kf, op, u, ntets_sample, reps=2):
     """Oracle port (C restatement of kernels.apply_scaling_3d) on the host
     cores over a bounded sample of macro elements of the same workload."""
@@ -396,7 +407,8 @@ def cpu_baseline(grid, kf, op, u, ntets_sample, reps=2):
         ts.append(time.perf_counter() - t0)
     t = min(ts)
     return {"value": round(T * grid.nodes_per_volume / t / 1e9, 4), "unit": "GDoF/s",
-            "cores": threads, "kind": "port",
+            "cores": threads, "kind": "port", "cpu_model": cpu_model(),
+            "host_cpus": os.cpu_count(),
             "sample": f"{T} of {grid.macro.n_elements} macro tets (level {grid.level}) "
                       f"per step, best of {reps}, volume rows, all host threads"}
 
@@ -438,7 +450,8 @@ def run_reference(args):
             "config": {"workload": f"config 5 per GPU: 4x4x1 Kuhn-cube slab, 96 macro tets, "
                                    f"level {args.level}", "level": args.level},
             "cpu_baseline": {"value": round(val, 4), "unit": "GDoF/s", "cores": threads,
-                             "kind": "port",
+                             "kind": "port", "cpu_model": cpu_model(),
+                             "host_cpus": os.cpu_count(),
                              "sample": f"{T} macro tets of level {args.level} per step "
                                        "(volume rows), C restatement of "
                                        "kernels.apply_scaling_3d, one thread per core"},
