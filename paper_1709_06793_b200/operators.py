@@ -498,7 +498,7 @@ class Operator:
             if pool is None:
                 import os
                 from concurrent.futures import ThreadPoolExecutor
-                pool = P["pool"] = ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1))
+                pool = P["pool"] = ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 1))
             views = [(src, self._staging(key).numpy()) for src, _, key in srcs]
             for ci, (a, b) in enumerate(chunks):
                 if b > a:
