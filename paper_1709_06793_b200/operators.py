@@ -315,12 +315,12 @@ class Operator:
                      push=None):
         """Device-resident A u (or f - A u when f is given), torch tensors.
 
-        Order: ghost update, then the volume rows and the surface + Dirichlet
-        rows.  The surface rows - disjoint from the volume rows - run right
-        after the ghost update on a side stream, followed by
+        Order: ghost update, volume rows, surface + Dirichlet rows.  With
         ``after_surface(out)`` (the sharded operator's interface exchange)
-        when given, concurrently with the volume kernel; the side stream
-        joins before returning.
+        the surface rows - disjoint from the volume rows - run right after
+        the ghost update on a side stream followed by the callable,
+        concurrently with the volume kernel; the side stream joins before
+        returning.
         ``volume_events``: optional (start, end) CUDA events recorded around
         the volume kernel on the launching stream (bench.py)."""
         D = self._device()
@@ -333,12 +333,12 @@ class Operator:
         flags = self._vol_flags(residual=f is not None)
         res = flags & _lib.FLAG_RESIDUAL
         fp = f.data_ptr() if f is not None else None
-        # surface rows on a side stream, concurrently with the volume kernel
-        # (always with an exchange hook; on one GPU from level 6 on, where
-        # the face-tiled rows overlap the latency-bound volume kernel:
-        # 1.938 -> 1.913 ms per config-5 apply, tools/overlap_probe.py)
-        concurrent = self.surface_mode != "matrix-free" and (
-            after_surface is not None or self.grid.n >= 64)
+        # surface rows on a side stream, concurrently with the volume kernel,
+        # when an exchange hook follows them (N > 1).  On one GPU the overlap
+        # gains 0.6-1.3% per config-5 apply (tools/overlap_probe.py) but
+        # slows the volume kernel itself by sharing the SMs (1.63 -> 1.82
+        # ms), so the sequential order is kept there.
+        concurrent = self.surface_mode != "matrix-free" and after_surface is not None
         # the surface rows read shell values from the ghost layer: refresh first
         check(lib.hhg_ghost_update(dg.ref, du.data_ptr(), st), "ghost_update")
         if concurrent:
