@@ -330,7 +330,19 @@ typedef struct hhg_surface_gs {
   int32_t *ent_col;           /* [nent] global ids (filled by _prepare)       */
   double *ent_val;            /* [nent] weights (filled by _prepare)          */
   double *row_diag;           /* [nrows] diagonals (filled by _prepare)       */
+  /* optional level-ordered copy for the one-cluster sweep (filled by
+   * hhg_smooth_surface_slots; NULL = not built): slot e is row
+   * level_rows[e]; its first HHG_SURF_SLOT_PF entries are stored
+   * slot-interleaved (entry m of slot e at m * nslots + e), so a thread
+   * reads its next row with no dependent loads */
+  int64_t nslots;             /* = nrows                                      */
+  int64_t *slot_gid;          /* [nslots] global id of the row                */
+  int32_t *slot_cnt;          /* [nslots] entries of the row                  */
+  double *slot_diag;          /* [nslots]                                     */
+  int32_t *slot_col;          /* [HHG_SURF_SLOT_PF * nslots]                  */
+  double *slot_val;           /* [HHG_SURF_SLOT_PF * nslots]                  */
 } hhg_surface_gs;
+#define HHG_SURF_SLOT_PF 24
 
 /* apply / residual of the surface rows (+ Dirichlet rows) from the rows
  * precomputed by hhg_smooth_surface_prepare; bitwise the matrix-free
@@ -374,7 +386,13 @@ int hhg_ipc_close_handle(void *ptr);
 
 int hhg_smooth_surface_prepare(const hhg_grid *g, const hhg_surface *s,
                                const hhg_surface_gs *gs, void *stream);
-/* every level of the surface sweep in one cooperative launch */
+/* fill gs->slot_* (allocated by the caller) from the level schedule and
+ * the prepared rows; call after _prepare and whenever they change */
+int hhg_smooth_surface_slots(const hhg_grid *g, const hhg_surface *s,
+                             const hhg_surface_gs *gs, void *stream);
+/* every level of the surface sweep in one launch: one thread-block cluster
+ * with a cluster barrier between levels when gs->slot_gid is set, else a
+ * cooperative grid with grid barriers */
 int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s,
                            const hhg_surface_gs *gs, double omega, double *u,
                            const double *f, void *stream);

@@ -75,7 +75,12 @@ class HhgFace(ctypes.Structure):
 
 class HhgSurfaceGS(ctypes.Structure):
     _fields_ = [("level_rows", vp), ("level_ptr", vp), ("nlev", ctypes.c_int64),
-                ("ent_ptr", vp), ("ent_col", vp), ("ent_val", vp), ("row_diag", vp)]
+                ("ent_ptr", vp), ("ent_col", vp), ("ent_val", vp), ("row_diag", vp),
+                ("nslots", ctypes.c_int64), ("slot_gid", vp), ("slot_cnt", vp),
+                ("slot_diag", vp), ("slot_col", vp), ("slot_val", vp)]
+
+
+SURF_SLOT_PF = 24   # HHG_SURF_SLOT_PF
 
 
 # name -> (restype, argtypes); every symbol of include/hhg_b200.h
@@ -115,6 +120,9 @@ EXPORTS = {
                                              ctypes.POINTER(HhgSurface),
                                              ctypes.POINTER(HhgSurfaceGS), ctypes.c_int,
                                              vp, vp, vp, vp]),
+    "hhg_smooth_surface_slots": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
+                                                ctypes.POINTER(HhgSurface),
+                                                ctypes.POINTER(HhgSurfaceGS), vp]),
     "hhg_smooth_surface_all": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
                                               ctypes.POINTER(HhgSurface),
                                               ctypes.POINTER(HhgSurfaceGS), ctypes.c_double,

@@ -359,21 +359,31 @@ static int device_capacity(K kern, int threads, std::map<int, int> &cache) {
 #define HHG_GS_CLUSTER 4         // CTAs per element of the cluster sweeps (0: off)
 #endif
 
+// CTAs per element of the cluster volume sweeps (HHG_GS_CLUSTER_N overrides;
+// > 8 needs the non-portable opt-in)
+static int gs_cluster() {
+  static const int v = [] {
+    const char *e = getenv("HHG_GS_CLUSTER_N");
+    return e ? atoi(e) : HHG_GS_CLUSTER;
+  }();
+  return v;
+}
+
 template <int VAR>
 static int launch_gs_volume(GSDesc G, cudaStream_t st) {
-  if (HHG_GS_CLUSTER > 0 && G.n >= 16) {
+  if (gs_cluster() > 0 && G.n >= 16) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(G.ntets * HHG_GS_CLUSTER);
+    cfg.gridDim = dim3(G.ntets * gs_cluster());
     cfg.blockDim = dim3(gs_cluster_threads<VAR>());
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = HHG_GS_CLUSTER;
+    attr[0].val.clusterDim.x = gs_cluster();
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    G.cpt = HHG_GS_CLUSTER;
+    G.cpt = gs_cluster();
     g_launches.fetch_add(1, std::memory_order_relaxed);
     cudaError_t e = cudaLaunchKernelEx(&cfg, gs_volume_cluster_kernel<VAR>, G);
     if (e != cudaSuccess) {
@@ -884,7 +894,27 @@ static SurfGSDesc surf_gs_desc(const hhg_grid *g, const hhg_surface *s, const hh
   G.ent_col = gs->ent_col;
   G.ent_val = gs->ent_val;
   G.row_diag = gs->row_diag;
+  G.level_rows = reinterpret_cast<const long long *>(gs->level_rows);
+  G.nslots = gs->nslots;
+  G.slot_gid = reinterpret_cast<const long long *>(gs->slot_gid);
+  G.slot_cnt = gs->slot_cnt;
+  G.slot_col = gs->slot_col;
+  G.slot_diag = gs->slot_diag;
+  G.slot_val = gs->slot_val;
   return G;
+}
+
+int hhg_smooth_surface_slots(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
+                             void *stream) {
+  if (gs->nslots <= 0) return HHG_OK;
+  if (!gs->slot_gid || !gs->slot_cnt || !gs->slot_diag || !gs->slot_col || !gs->slot_val ||
+      !gs->level_rows)
+    return HHG_ERR_ARG;
+  SurfGSDesc G = surf_gs_desc(g, s, gs, 1.0, nullptr, nullptr);
+  surface_slots_kernel<<<(int)((gs->nslots + 255) / 256), 256, 0, S(stream)>>>(
+      G, reinterpret_cast<long long *>(gs->slot_gid), gs->slot_cnt, gs->slot_diag, gs->slot_col,
+      gs->slot_val);
+  return check("surface_slots_kernel");
 }
 
 int hhg_smooth_surface_rows(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
@@ -924,27 +954,51 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_su
                            double omega, double *u, const double *f, void *stream) {
   if (g->n > HHG_MAX_N) return HHG_ERR_ARG;   // 32-bit lattice forms, 10-bit point codes
   if (gs->nlev <= 0) return HHG_OK;
-  SurfGSDesc G{};
-  G.s = surf_desc(g, s);
-  G.s.u = u;
-  G.s.f = f;
-  G.shell_gid = reinterpret_cast<const long long *>(g->shell_gid);
-  G.level_rows = reinterpret_cast<const long long *>(gs->level_rows);
-  G.omega = omega;
-  G.ent_ptr = reinterpret_cast<const long long *>(gs->ent_ptr);
-  G.ent_col = gs->ent_col;
-  G.ent_val = gs->ent_val;
-  G.row_diag = gs->row_diag;
+  SurfGSDesc G = surf_gs_desc(g, s, gs, omega, u, f);
+  const long long *lp = reinterpret_cast<const long long *>(gs->level_ptr);
+  int nl = (int)gs->nlev;
+  // narrow sweeps (mean level width <= 1024 rows: level 6, 7 grids): one
+  // 16-CTA thread-block cluster walks the levels, a cluster barrier between
+  // them (measured 8% faster than the grid barrier there); wider sweeps
+  // need the memory parallelism of the whole GPU: the cooperative grid.
+  // HHG_SURF_CLUSTER overrides: CTAs per cluster (> 8 needs the
+  // non-portable opt-in), 0 = always the cooperative grid.
+  static const int env_cl = [] {
+    const char *e = getenv("HHG_SURF_CLUSTER");
+    return e ? atoi(e) : -1;
+  }();
+  const long long mean_width = (s->nrows + gs->nlev - 1) / gs->nlev;
+  const int ncl = env_cl >= 0 ? env_cl : (mean_width <= 1024 ? 16 : 0);
+  if (ncl > 0 && gs->slot_gid && gs->nslots == s->nrows) {
+    if (ncl > 8)
+      cudaFuncSetAttribute(gs_surface_cluster_kernel,
+                           cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ncl);
+    cfg.blockDim = dim3(HHG_SURF_CT);
+    cfg.stream = S(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ncl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gs_surface_cluster_kernel, G, lp, nl);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "hhg_b200: gs_surface_cluster_kernel: %s\n", cudaGetErrorString(e));
+      return HHG_ERR_CUDA;
+    }
+    return HHG_OK;
+  }
   static std::map<int, int> caps;
   const int max_blocks = device_capacity(gs_surface_all_kernel, 64, caps);
   // spread each level over many SMs (a single SM's outstanding-miss limit
   // bounds a level to ~15 us); ~8 rows per 64-thread block
-  long long width = (s->nrows + gs->nlev - 1) / gs->nlev;
-  int blocks = (int)((width + 7) / 8);
+  int blocks = (int)((mean_width + 7) / 8);
   if (blocks < 8) blocks = 8;
   if (blocks > max_blocks) blocks = max_blocks;
-  const long long *lp = reinterpret_cast<const long long *>(gs->level_ptr);
-  int nl = (int)gs->nlev;
   void *args[] = {(void *)&G, (void *)&lp, (void *)&nl};
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaLaunchCooperativeKernel((void *)gs_surface_all_kernel, blocks, 64, args,
@@ -1031,25 +1085,53 @@ int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef, d
   if ((rc = check("skew_move_kernel"))) return rc;
   skew_move_kernel<0><<<mv, 256, 0, S(stream)>>>(G, f, fs);
   if ((rc = check("skew_move_kernel"))) return rc;
+  // CTAs per element: the most (<= 8) with which every element's cluster is
+  // co-resident in one wave (the sweep is latency-bound: more threads per
+  // hyperplane help, a second wave of elements does not); at least 4.
+  // HHG_GS_CLUSTER_N fixes it.
+  const bool nodal = variant == HHG_VAR_NODAL;
+  const void *kfn = nodal ? (const void *)gs_volume_skew_kernel<1>
+                          : (const void *)gs_volume_skew_kernel<0>;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(G.ntets * HHG_GS_CLUSTER);
   cfg.stream = S(stream);
+  cfg.blockDim = dim3(nodal ? gs_cluster_threads<1>() : gs_cluster_threads<0>());
+  cfg.dynamicSmemBytes = 8 * (G.n + 1) * sizeof(int);   // start-table ring
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = HHG_GS_CLUSTER;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  int cl = gs_cluster();
+  if (!getenv("HHG_GS_CLUSTER_N")) {
+    static std::map<std::tuple<int, int, int>, int> pick;
+    std::lock_guard<std::mutex> lock(g_cache_mu);
+    const auto key = std::make_tuple(current_device(), (int)nodal, G.ntets);
+    auto it = pick.find(key);
+    if (it == pick.end()) {
+      int best = 4;
+      for (int c = 8; c > 4; --c) {
+        cfg.gridDim = dim3(G.ntets * c);
+        attr[0].val.clusterDim.x = c;
+        int fit = 0;
+        if (cudaOccupancyMaxActiveClusters(&fit, kfn, &cfg) == cudaSuccess && fit >= G.ntets) {
+          best = c;
+          break;
+        }
+        cudaGetLastError();
+      }
+      it = pick.emplace(key, best).first;
+    }
+    cl = it->second;
+  }
+  cfg.gridDim = dim3(G.ntets * cl);
+  attr[0].val.clusterDim.x = cl;
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e;
-  if (variant == HHG_VAR_NODAL) {
-    cfg.blockDim = dim3(gs_cluster_threads<1>());
+  if (nodal)
     e = cudaLaunchKernelEx(&cfg, gs_volume_skew_kernel<1>, G, (const double *)us, fs, ks, start);
-  } else {
-    cfg.blockDim = dim3(gs_cluster_threads<0>());
+  else
     e = cudaLaunchKernelEx(&cfg, gs_volume_skew_kernel<0>, G, (const double *)us, fs, ks, start);
-  }
   if (e != cudaSuccess) {
     fprintf(stderr, "hhg_b200: gs_volume_skew_kernel: %s\n", cudaGetErrorString(e));
     return HHG_ERR_CUDA;

@@ -368,10 +368,6 @@ __global__ void skew_move_kernel(GSDesc D, const double *__restrict__ src,
   else dst[g] = src[sk];
 }
 
-#ifndef HHG_GS_SKEW_P
-#define HHG_GS_SKEW_P 1          // points per thread with loads in flight together (2: slower, registers)
-#endif
-
 template <int VAR>
 __global__ void __launch_bounds__(gs_cluster_threads<VAR>())
 gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ fs,
@@ -400,14 +396,26 @@ gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ f
   const double *ke = ks + (long long)t * D.nvol;
   const int stride = cpt * blockDim.x;
   const int first = part * blockDim.x + threadIdx.x;
+  // ring of the start-table rows of hyperplanes h-3 .. h+3 (row hq in slot
+  // hq & 7): the neighbour positions come from shared memory, not from a
+  // dependent L2 load per point; row h+4 is staged during hyperplane h
+  extern __shared__ int st_ring[];
+  const int srl = n + 1;
+  auto stage_row = [&](int hq) {
+    if (hq > hmax) return;
+    const int *src = start + (hq - hmin) * srl;
+    int *dst = st_ring + (hq & 7) * srl;
+    for (int x = threadIdx.x; x < srl; x += blockDim.x) dst[x] = __ldg(src + x);
+  };
+  for (int hq = hmin; hq <= hmin + 3; ++hq) stage_row(hq);
+  __syncthreads();
   // a point's loads (neighbour values and coefficients, own old value, f)
-  // and its update, split so that two points' loads are in flight together
+  // and its update
   struct Pt {
     double2 q[14];
     double k0, fv, old;
   };
-  auto gather = [&](int h, int e, Pt &X) {
-    const int code = __ldg(D.hp_code + e);
+  auto gather = [&](int h, int e, int code, Pt &X) {
     const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
     const IncPlanes P = inc_planes(n, k);
 #pragma unroll
@@ -417,7 +425,7 @@ gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ f
       const bool inner = qi >= 1 && qj >= 1 && qk >= 1 && qi + qj + qk <= n - 1;
       if (inner) {
         const int hq = h + di + 2 * dj + 3 * dk;
-        const int pos = __ldg(start + (hq - hmin) * (n + 1) + qk) + qj;
+        const int pos = st_ring[(hq & 7) * srl + qk] + qj;
         X.q[d] = make_double2(__ldcg(ue + pos), __ldg(ke + pos));
       } else {
         int off;
@@ -447,23 +455,23 @@ gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ f
     __stcg(ue + e, dadd(dmul(dsub(1.0, omega), X.old),
                         ddiv(dmul(omega, dsub(X.fv, acc)), diag)));
   };
+  // the point code of the thread's next point is loaded one point ahead
+  // (for the first point of the next hyperplane: before the barrier)
+  int ha = __ldg(D.hp_ptr), hb = __ldg(D.hp_ptr + 1);
+  int code = ha + first < hb ? __ldg(D.hp_code + ha + first) : 0;
   for (int h = hmin; h <= hmax; ++h) {
-    const int ha = __ldg(D.hp_ptr + h - hmin), hb = __ldg(D.hp_ptr + h + 1 - hmin);
-    for (int e = ha + first; e < hb; e += HHG_GS_SKEW_P * stride) {
-      if constexpr (HHG_GS_SKEW_P >= 2 && VAR == 0) {
-        Pt a, b;
-        gather(h, e, a);
-        const bool two = e + stride < hb;
-        if (two) gather(h, e + stride, b);
-        finish(e, a);
-        if (two) finish(e + stride, b);
-      } else {
-        for (int x = 0, ee = e; x < HHG_GS_SKEW_P && ee < hb; ++x, ee += stride) {
-          Pt a;
-          gather(h, ee, a);
-          finish(ee, a);
-        }
-      }
+    for (int e = ha + first; e < hb; e += stride) {
+      const int code_next = e + stride < hb ? __ldg(D.hp_code + e + stride) : 0;
+      Pt a;
+      gather(h, e, code, a);
+      finish(e, a);
+      code = code_next;
+    }
+    stage_row(h + 4);
+    if (h < hmax) {
+      ha = hb;
+      hb = __ldg(D.hp_ptr + h + 2 - hmin);
+      code = ha + first < hb ? __ldg(D.hp_code + ha + first) : 0;
     }
     cluster_sync_all();
   }
@@ -481,6 +489,11 @@ struct SurfGSDesc {
   const long long *ent_ptr;
   int *ent_col;
   double *ent_val, *row_diag;
+  // level-ordered slots (gs_surface_cluster_kernel)
+  long long nslots;
+  const long long *slot_gid;
+  const int *slot_cnt, *slot_col;
+  const double *slot_diag, *slot_val;
 };
 
 __device__ __forceinline__ long long point_gid(const SurfDesc &D,
@@ -924,6 +937,123 @@ gs_surface_all_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
       }
     }
     grid.sync();
+  }
+}
+
+// The same sweep on ONE thread-block cluster, from the level-ordered slots
+// (hhg_surface_gs.slot_*): a level's rows are spread over the cluster's
+// CTAs; between levels a split hardware cluster barrier (arrive.release,
+// then wait.acquire; cluster scope) replaces the grid barrier, and the
+// static part of each thread's next row (id, count, diagonal, f, column
+// ids: one coalesced load per field, no dependent address chain) is fetched
+// between the arrive and the wait, so it overlaps the barrier.  After the
+// wait one round of loads remains on the level's critical path: the
+// neighbour values (through L2: other CTAs write them) and the weights.
+// Entries, order and arithmetic are gs_surface_row_csr's: bitwise the same.
+constexpr int kSlotPF = HHG_SURF_SLOT_PF;
+struct SlotRow {
+  long long gid;
+  int cnt;
+  double diag, fv;
+  int col[kSlotPF];
+};
+
+__device__ __forceinline__ void slot_prefetch(const SurfGSDesc &G, long long e, SlotRow &p) {
+  const long long ns = G.nslots;
+  p.gid = __ldg(G.slot_gid + e);
+  p.cnt = __ldg(G.slot_cnt + e);
+  p.diag = __ldg(G.slot_diag + e);
+#pragma unroll
+  for (int m = 0; m < kSlotPF; ++m)      // padded slots hold column 0
+    p.col[m] = __ldg(G.slot_col + m * ns + e);
+  p.fv = __ldg(G.s.f + p.gid);
+}
+
+__device__ __forceinline__ void slot_finish(const SurfGSDesc &G, long long e, const SlotRow &p) {
+  double *u = const_cast<double *>(G.s.u);
+  // weights (static, independent) in the same round as the neighbours
+  const long long ns = G.nslots;
+  double x[kSlotPF], w[kSlotPF];
+#pragma unroll
+  for (int m = 0; m < kSlotPF; ++m)
+    if (m < p.cnt) {
+      x[m] = __ldcg(u + (unsigned)p.col[m]);
+      w[m] = __ldg(G.slot_val + m * ns + e);
+    }
+  const double old = __ldcg(u + p.gid);
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < kSlotPF; ++m)
+    if (m < p.cnt) acc = dadd(acc, dmul(w[m], x[m]));
+  if (p.cnt > kSlotPF) {               // long (edge / vertex) rows: the rest
+    const long long r = __ldg(G.level_rows + e);
+    const long long e1 = __ldg(G.ent_ptr + r + 1);
+#pragma unroll 1
+    for (long long q = __ldg(G.ent_ptr + r) + kSlotPF; q < e1; q += 8) {
+      int cl[8];
+      double w[8], xv[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (q + m < e1) {
+          cl[m] = __ldg(G.ent_col + q + m);
+          w[m] = __ldg(G.ent_val + q + m);
+        }
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (q + m < e1) xv[m] = __ldcg(u + (unsigned)cl[m]);
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        if (q + m < e1) acc = dadd(acc, dmul(w[m], xv[m]));
+    }
+  }
+  if (p.diag == 0.0) atomicOr(&g_status, 1);
+  const double om = G.omega;
+  u[p.gid] = dadd(dmul(dsub(1.0, om), old), ddiv(dmul(om, dsub(p.fv, acc)), p.diag));
+}
+
+__global__ void surface_slots_kernel(SurfGSDesc G, long long *gid, int *cnt, double *diag,
+                                     int *col, double *val) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long ns = G.nslots;
+  if (e >= ns) return;
+  const long long r = G.level_rows[e];
+  const long long e0 = G.ent_ptr[r], c = G.ent_ptr[r + 1] - e0;
+  gid[e] = G.s.rows[r];
+  cnt[e] = (int)c;
+  diag[e] = G.row_diag[r];
+  for (int m = 0; m < kSlotPF; ++m) {
+    col[m * ns + e] = m < c ? G.ent_col[e0 + m] : 0;
+    val[m * ns + e] = m < c ? G.ent_val[e0 + m] : 0.0;
+  }
+}
+
+#ifndef HHG_SURF_CT
+#define HHG_SURF_CT 256          // threads per CTA of the cluster surface sweep
+#endif
+__global__ void __launch_bounds__(HHG_SURF_CT)
+gs_surface_cluster_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
+  const long long nb = cluster_nctas();
+  const long long tid = threadIdx.x * nb + cluster_ctarank();
+  const long long nth = nb * blockDim.x;
+  SlotRow pf;
+  bool have = nlev > 0 && level_ptr[0] + tid < level_ptr[1];
+  if (have) slot_prefetch(G, level_ptr[0] + tid, pf);
+  for (int lv = 0; lv < nlev; ++lv) {
+    const long long b = level_ptr[lv + 1];
+    // one inlined copy of each step (register pressure)
+    for (long long e = level_ptr[lv] + tid; e < b; e += nth) {
+      if (!have) slot_prefetch(G, e, pf);
+      have = false;
+      slot_finish(G, e, pf);
+    }
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    have = false;
+    if (lv + 1 < nlev) {
+      const long long e = b + tid;
+      have = e < level_ptr[lv + 2];
+      if (have) slot_prefetch(G, e, pf);
+    }
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   }
 }
 

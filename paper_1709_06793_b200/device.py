@@ -525,8 +525,24 @@ class DeviceSurface:
             torch = require_cuda()
             order, ptr, nlev = self.st.gs_levels()
             keep = [torch.as_tensor(order, device="cuda"), torch.as_tensor(ptr, device="cuda")]
-            c["desc"].level_rows, c["desc"].level_ptr = keep[0].data_ptr(), keep[1].data_ptr()
-            c["desc"].nlev = nlev
-            c["keep"] += keep
+            d = c["desc"]
+            d.level_rows, d.level_ptr = keep[0].data_ptr(), keep[1].data_ptr()
+            d.nlev = nlev
+            # level-ordered slots of the one-cluster sweep
+            from ._lib import SURF_SLOT_PF, check
+            ns = len(order)
+            slots = [torch.empty(max(ns, 1), dtype=torch.int64, device="cuda"),
+                     torch.empty(max(ns, 1), dtype=torch.int32, device="cuda"),
+                     torch.empty(max(ns, 1), dtype=torch.float64, device="cuda"),
+                     torch.empty(max(ns, 1) * SURF_SLOT_PF, dtype=torch.int32, device="cuda"),
+                     torch.empty(max(ns, 1) * SURF_SLOT_PF, dtype=torch.float64,
+                                 device="cuda")]
+            d.nslots = ns
+            (d.slot_gid, d.slot_cnt, d.slot_diag, d.slot_col,
+             d.slot_val) = (x.data_ptr() for x in slots)
+            check(lib.hhg_smooth_surface_slots(dg.ref, self.ref, c["ref"],
+                                               torch.cuda.current_stream().cuda_stream),
+                  "smooth_surface_slots")
+            c["keep"] += keep + slots
             self._levels = nlev
         return {"ref": c["ref"], "nlev": self._levels}
