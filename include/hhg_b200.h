@@ -398,15 +398,22 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s,
                            const double *f, void *stream);
 int hhg_smooth_volume(const hhg_grid *g, int variant, const double *coef,
                       double omega, double *u, const double *f, void *stream);
-/* the same volume sweep in a hyperplane-major ("skewed") copy of the
- * element interiors: u and f are gathered into us / fs (ntets * nvol
- * doubles each, caller-owned), swept with coalesced accesses, and u is
- * scattered back; ks is the skewed coefficient from hhg_skew_coefficient
- * (static per operator).  Bitwise hhg_smooth_volume. */
+/* the same volume sweep in a hyperplane-major ("skewed") copy of each
+ * element's whole lattice: u with its ghost (boundary) values is gathered
+ * into us and ks holds the coefficient (ntets * L doubles each, L = lattice
+ * points per element; ks filled once per operator by hhg_skew_coefficient),
+ * f into fs (ntets * nvol doubles); the interior is swept with coalesced,
+ * branch-free accesses and scattered back into u.  Bitwise
+ * hhg_smooth_volume.  Caller-owned buffers.  flags (later sweeps of one
+ * smoothing): HHG_SKEW_F_CURRENT - fs already holds this f;
+ * HHG_SKEW_U_CURRENT - the interior of us equals u's (only the boundary
+ * values are refreshed from the ghost shell). */
+#define HHG_SKEW_F_CURRENT 1
+#define HHG_SKEW_U_CURRENT 2
 int hhg_skew_coefficient(const hhg_grid *g, double *ks, void *stream);
 int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef,
                            double omega, double *u, const double *f, double *us,
-                           double *fs, const double *ks, void *stream);
+                           double *fs, const double *ks, int flags, void *stream);
 
 /* ---------------------------------------------------------------------
  * (3) tensor-coefficient operators, M = 6 component fields

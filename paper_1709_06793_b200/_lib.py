@@ -131,7 +131,8 @@ EXPORTS = {
                                          ctypes.c_double, vp, vp, vp]),
     "hhg_skew_coefficient": (ctypes.c_int, [ctypes.POINTER(HhgGrid), vp, vp]),
     "hhg_smooth_volume_skew": (ctypes.c_int, [ctypes.POINTER(HhgGrid), ctypes.c_int, vp,
-                                              ctypes.c_double, vp, vp, vp, vp, vp, vp]),
+                                              ctypes.c_double, vp, vp, vp, vp, vp,
+                                              ctypes.c_int, vp]),
     "hhg_apply_scaling_tensor_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp,
                                                    ctypes.c_int64, vp, vp, vp]),
     "hhg_apply_nodal_tensor_3d": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, ctypes.c_int64,

@@ -471,10 +471,18 @@ int hhg_apply_stored_3d(int64_t n, const int64_t *, const double *v, const doubl
 // interior points of each hyperplane h = i + 2j + 3k (host-built once per n)
 struct Hyperplanes {
   int *ptr = nullptr, *code = nullptr;
-  int *start = nullptr;   // [(h - 6) (n + 1) + k]: skewed position of (i, j, k) = start + j
+  // the whole (n+1)-lattice (interior + boundary points) in hyperplane
+  // order - h = i + 2j + 3k (0 .. 3n), then k, then j: position of (i, j, k)
+  // = xstart[h (n + 1) + k] + j; xcode = the point codes in that order
+  int *xstart = nullptr, *xcode = nullptr;
+  // the boundary (ghost) points: code and position in that order
+  int *bcode = nullptr, *bpos = nullptr;
+  int nb = 0;
 };
 
-static int hyperplanes(int n, const int **ptr, const int **code, const int **start = nullptr) {
+static int hyperplanes(int n, const int **ptr, const int **code, const int **xstart = nullptr,
+                       const int **xcode = nullptr, const int **bcode = nullptr,
+                       const int **bpos = nullptr, int *nb = nullptr) {
   static std::map<std::pair<int, int>, Hyperplanes> cache;
   std::lock_guard<std::mutex> lock(g_cache_mu);
   const auto key = std::make_pair(current_device(), n);
@@ -491,34 +499,43 @@ static int hyperplanes(int n, const int **ptr, const int **code, const int **sta
         }
     }
     if (hmax >= hmin) p[hmax - hmin + 1] = (int)c.size();
-    // skewed (hyperplane-major) position of interior point (i, j, k): its
-    // index in the list above = start[(h - 6)(n + 1) + k] + j
-    std::vector<int> st(std::max(hmax - hmin + 1, 1) * (n + 1), 0);
-    for (int h = hmin; h <= hmax; ++h) {
-      int pos = p[h - hmin];
-      for (int k = 1; k <= n - 3; ++k) {
-        int jmin = -1, cnt = 0;
-        for (int j = 1; j <= n - 2 - k; ++j) {
+    std::vector<int> xs((3 * n + 1) * (n + 1), 0), xc, bc, bp;
+    for (int h = 0; h <= 3 * n; ++h)
+      for (int k = 0; k <= n; ++k) {
+        int jmin = -1;
+        for (int j = 0; j <= n - k; ++j) {
           const int i = h - 2 * j - 3 * k;
-          if (i >= 1 && i + j + k <= n - 1) {
-            if (jmin < 0) jmin = j;
-            ++cnt;
+          if (i >= 0 && i + j + k <= n) {
+            if (jmin < 0) {
+              jmin = j;
+              xs[h * (n + 1) + k] = (int)xc.size() - j;
+            }
+            if (!(i >= 1 && j >= 1 && k >= 1 && i + j + k <= n - 1)) {
+              bc.push_back(i | (j << 10) | (k << 20));
+              bp.push_back((int)xc.size());
+            }
+            xc.push_back(i | (j << 10) | (k << 20));
           }
         }
-        st[(h - hmin) * (n + 1) + k] = jmin < 0 ? 0 : pos - jmin;
-        pos += cnt;
       }
-    }
     Hyperplanes hp;
     int rc = upload(p, &hp.ptr);
     if (!rc) rc = upload(c, &hp.code);
-    if (!rc) rc = upload(st, &hp.start);
+    if (!rc) rc = upload(xs, &hp.xstart);
+    if (!rc) rc = upload(xc, &hp.xcode);
+    if (!rc) rc = upload(bc, &hp.bcode);
+    if (!rc) rc = upload(bp, &hp.bpos);
     if (rc) return rc;
+    hp.nb = (int)bc.size();
     it = cache.emplace(key, hp).first;
   }
   *ptr = it->second.ptr;
   *code = it->second.code;
-  if (start) *start = it->second.start;
+  if (xstart) *xstart = it->second.xstart;
+  if (xcode) *xcode = it->second.xcode;
+  if (bcode) *bcode = it->second.bcode;
+  if (bpos) *bpos = it->second.bpos;
+  if (nb) *nb = it->second.nb;
   return HHG_OK;
 }
 
@@ -1063,28 +1080,38 @@ int hhg_skew_coefficient(const hhg_grid *g, double *ks, void *stream) {
   if (g->n > HHG_MAX_N) return HHG_ERR_ARG;
   if (g->n < 4 || g->nvol == 0) return HHG_OK;
   GSDesc G = gs_grid_desc(g, HHG_VAR_SCALING, nullptr, 1.0, nullptr, nullptr);
-  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code);
+  const int *xstart = nullptr, *xcode = nullptr;
+  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code, &xstart, &xcode);
   if (rc) return rc;
-  skew_move_kernel<2><<<dim3((int)((g->nvol + 255) / 256), g->ntets), 256, 0, S(stream)>>>(
-      G, nullptr, ks);
+  skew_move_kernel<2><<<dim3((int)((G.L + 255) / 256), g->ntets), 256, 0, S(stream)>>>(
+      G, xcode, nullptr, ks);
   return check("skew_move_kernel");
 }
 
 int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef, double omega,
                            double *u, const double *f, double *us, double *fs,
-                           const double *ks, void *stream) {
+                           const double *ks, int flags, void *stream) {
   if (g->n > HHG_MAX_N) return HHG_ERR_ARG;
   if (g->n < 4 || g->nvol == 0) return HHG_OK;
   if (!us || !fs || !ks) return HHG_ERR_ARG;
   GSDesc G = gs_grid_desc(g, variant, coef, omega, u, f);
-  const int *start = nullptr;
-  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code, &start);
+  const int *xstart = nullptr, *xcode = nullptr, *bcode = nullptr, *bpos = nullptr;
+  int nb = 0;
+  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code, &xstart, &xcode, &bcode, &bpos, &nb);
   if (rc) return rc;
-  const dim3 mv((int)((g->nvol + 255) / 256), g->ntets);
-  skew_move_kernel<0><<<mv, 256, 0, S(stream)>>>(G, u, us);
-  if ((rc = check("skew_move_kernel"))) return rc;
-  skew_move_kernel<0><<<mv, 256, 0, S(stream)>>>(G, f, fs);
-  if ((rc = check("skew_move_kernel"))) return rc;
+  const dim3 mx((int)((G.L + 255) / 256), g->ntets);
+  if (flags & HHG_SKEW_U_CURRENT) {     // interior of us current: ghost values only
+    skew_boundary_kernel<<<dim3((nb + 255) / 256, g->ntets), 256, 0, S(stream)>>>(
+        G, bcode, bpos, nb, us);
+    if ((rc = check("skew_boundary_kernel"))) return rc;
+  } else {
+    skew_move_kernel<0><<<mx, 256, 0, S(stream)>>>(G, xcode, u, us);
+    if ((rc = check("skew_move_kernel"))) return rc;
+  }
+  if (!(flags & HHG_SKEW_F_CURRENT)) {
+    skew_f_kernel<<<dim3((int)((g->nvol + 255) / 256), g->ntets), 256, 0, S(stream)>>>(G, f, fs);
+    if ((rc = check("skew_f_kernel"))) return rc;
+  }
   // CTAs per element: the most (<= 8) with which every element's cluster is
   // co-resident in one wave (the sweep is latency-bound: more threads per
   // hyperplane help, a second wave of elements does not); at least 4.
@@ -1129,14 +1156,14 @@ int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef, d
   g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e;
   if (nodal)
-    e = cudaLaunchKernelEx(&cfg, gs_volume_skew_kernel<1>, G, (const double *)us, fs, ks, start);
+    e = cudaLaunchKernelEx(&cfg, gs_volume_skew_kernel<1>, G, us, (const double *)fs, ks, xstart);
   else
-    e = cudaLaunchKernelEx(&cfg, gs_volume_skew_kernel<0>, G, (const double *)us, fs, ks, start);
+    e = cudaLaunchKernelEx(&cfg, gs_volume_skew_kernel<0>, G, us, (const double *)fs, ks, xstart);
   if (e != cudaSuccess) {
     fprintf(stderr, "hhg_b200: gs_volume_skew_kernel: %s\n", cudaGetErrorString(e));
     return HHG_ERR_CUDA;
   }
-  skew_move_kernel<1><<<mv, 256, 0, S(stream)>>>(G, us, u);
+  skew_move_kernel<1><<<mx, 256, 0, S(stream)>>>(G, xcode, us, u);
   return check("skew_move_kernel");
 }
 

@@ -337,42 +337,80 @@ gs_volume_cluster_kernel(GSDesc D) {
   }
 }
 
-// Skewed (hyperplane-major) form of the volume sweep.  The interior points
-// of each element are stored in hyperplane order - h = i + 2j + 3k, then k,
-// then j - so one hyperplane is a contiguous run and the neighbours of
-// consecutive points of a run are consecutive points of the neighbouring
-// runs (direction d moves h by di + 2dj + 3dk): every load and store of the
-// sweep is coalesced.  u and f are gathered into this order before the
-// sweep and u scattered back after it (skew_move_kernel); k is gathered once
-// per operator (static).  Same points per hyperplane, same arithmetic as
-// gs_volume_kernel: bitwise the lexicographic sweep.
-//   MODE 0: dst[t nvol + e] = src[vol_start[t] + vrank(e)]   (gather)
-//   MODE 1: dst[vol_start[t] + vrank(e)] = src[t nvol + e]   (scatter)
-//   MODE 2: dst[t nvol + e] = kc[t L + lattice(e)]          (coefficient)
+// Skewed (hyperplane-major) form of the volume sweep.  Each element's whole
+// (n+1)-lattice - interior points and the boundary points the ghost shell
+// holds - is stored in hyperplane order (h = i + 2j + 3k, then k, then j;
+// position xstart[h (n+1) + k] + j), u and the coefficient k as separate
+// copies (us, ks: ntets * L).  One hyperplane is a contiguous run, the
+// neighbours of consecutive points of a run are consecutive points of the
+// neighbouring runs (direction d moves h by di + 2dj + 3dk), and - with the
+// boundary layer in the same array - every neighbour of every interior
+// point is addressed the same way: no bounds tests, no ghost branch, no
+// divergence.  u (with the ghost values) is moved in before the sweep and
+// the interior back after it (a separate pass: storing each new value into
+// the global vector from the sweep - scattered 8-byte stores - measured
+// 1.5x slower at level 8), f (interior order of the hyperplane lists) once
+// per smoothing call, k once per operator.  Same points per
+// hyperplane, same arithmetic as gs_volume_kernel: bitwise the
+// lexicographic sweep.
+//   MODE 0: dst[t L + p] = u or ghost value of lattice point p (gather)
+//   MODE 1: u[interior p] = src[t L + p]                      (scatter)
+//   MODE 2: dst[t L + p] = kc[t L + lattice(p)]               (coefficient)
+// (skewed order on the write side of the gathers: the scattered 8-byte
+// reads are L2 hits - one element's block is ~23 MB at level 8 - while
+// scattered partial-sector writes would cost DRAM fills)
 template <int MODE>
-__global__ void skew_move_kernel(GSDesc D, const double *__restrict__ src,
-                                 double *__restrict__ dst) {
+__global__ void skew_move_kernel(GSDesc D, const int *__restrict__ xcode,
+                                 const double *__restrict__ src, double *__restrict__ dst) {
+  const int t = blockIdx.y;
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= D.L) return;
+  const int n = D.n;
+  const int code = __ldg(xcode + p);
+  const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+  const long long sk = (long long)t * D.L + p;
+  if (MODE == 2) {
+    dst[sk] = __ldg(D.kc + (long long)t * D.L + lbase32(n, k, j) + i);
+    return;
+  }
+  if (MODE == 0) {
+    bool ghost;
+    GSDesc E = D;
+    E.u = const_cast<double *>(src);
+    dst[sk] = __ldg(gs_addr(E, t, i, j, k, ghost));
+  } else if (i >= 1 && j >= 1 && k >= 1 && i + j + k <= n - 1) {
+    dst[D.vol_start[t] + lbase32(n - 4, k - 1, j - 1) + i - 1] = src[sk];
+  }
+}
+
+// refresh the boundary (ghost) points of us only: the interior is current
+// (the previous sweep of the same smoothing left it equal to u)
+__global__ void skew_boundary_kernel(GSDesc D, const int *__restrict__ bcode,
+                                     const int *__restrict__ bpos, int nb, double *us) {
+  const int t = blockIdx.y;
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  const int code = __ldg(bcode + b);
+  const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+  bool ghost;
+  us[(long long)t * D.L + __ldg(bpos + b)] = __ldg(gs_addr(D, t, i, j, k, ghost));
+}
+
+// f in the order of the hyperplane lists (interior points only)
+__global__ void skew_f_kernel(GSDesc D, const double *__restrict__ f, double *__restrict__ fs) {
   const int t = blockIdx.y;
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (e >= D.nvol) return;
   const int n = D.n;
   const int code = __ldg(D.hp_code + e);
   const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
-  const long long sk = (long long)t * D.nvol + e;
-  if (MODE == 2) {
-    dst[sk] = __ldg(D.kc + (long long)t * D.L + lbase32(n, k, j) + i);
-    return;
-  }
-  const long long g = D.vol_start[t] + lbase32(n - 4, k - 1, j - 1) + i - 1;
-  if (MODE == 0) dst[sk] = __ldg(src + g);
-  else dst[g] = src[sk];
+  fs[(long long)t * D.nvol + e] = __ldg(f + D.vol_start[t] + lbase32(n - 4, k - 1, j - 1) + i - 1);
 }
 
 template <int VAR>
 __global__ void __launch_bounds__(gs_cluster_threads<VAR>())
-gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ fs,
-                      const double *__restrict__ ks, const int *__restrict__ start) {
-  double *us = const_cast<double *>(us_c);
+gs_volume_skew_kernel(GSDesc D, double *us, const double *__restrict__ fs,
+                      const double *__restrict__ ks, const int *__restrict__ xstart) {
   const int cpt = (int)cluster_nctas();
   const int t = blockIdx.x / cpt;
   const int part = (int)cluster_ctarank();
@@ -385,75 +423,55 @@ gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ f
   } else {
     for (int e = threadIdx.x; e < 72; e += blockDim.x)
       sfac[e] = D.coef[(long long)t * D.coef_stride + e];
-    __syncthreads();
   }
   const double omega = D.omega;
   const int hmin = 6, hmax = 3 * n - 6;
-  const double *kt = D.kc + (long long)t * D.L;
-  const double *gt = D.ghost + (long long)t * D.S;
-  double *ue = us + (long long)t * D.nvol;
+  double *ue = us + (long long)t * D.L;
+  const double *ke = ks + (long long)t * D.L;
   const double *fe = fs + (long long)t * D.nvol;
-  const double *ke = ks + (long long)t * D.nvol;
   const int stride = cpt * blockDim.x;
   const int first = part * blockDim.x + threadIdx.x;
-  // ring of the start-table rows of hyperplanes h-3 .. h+3 (row hq in slot
-  // hq & 7): the neighbour positions come from shared memory, not from a
-  // dependent L2 load per point; row h+4 is staged during hyperplane h
+  // ring of the xstart rows of hyperplanes h-3 .. h+3 (row hq in slot
+  // hq & 7): positions come from shared memory; row h+4 is staged during
+  // hyperplane h
   extern __shared__ int st_ring[];
   const int srl = n + 1;
   auto stage_row = [&](int hq) {
-    if (hq > hmax) return;
-    const int *src = start + (hq - hmin) * srl;
+    if (hq > 3 * n) return;
+    const int *src = xstart + hq * srl;
     int *dst = st_ring + (hq & 7) * srl;
     for (int x = threadIdx.x; x < srl; x += blockDim.x) dst[x] = __ldg(src + x);
   };
-  for (int hq = hmin; hq <= hmin + 3; ++hq) stage_row(hq);
+  for (int hq = hmin - 3; hq <= hmin + 3; ++hq) stage_row(hq);
   __syncthreads();
-  // a point's loads (neighbour values and coefficients, own old value, f)
-  // and its update
-  struct Pt {
+  auto point = [&](int h, int e, int code) {
+    const int j = (code >> 10) & 1023, k = (code >> 20) & 1023;
     double2 q[14];
-    double k0, fv, old;
-  };
-  auto gather = [&](int h, int e, int code, Pt &X) {
-    const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
-    const IncPlanes P = inc_planes(n, k);
 #pragma unroll
     for (int d = 0; d < 14; ++d) {
       const int di = c_dirs_h(d, 0), dj = c_dirs_h(d, 1), dk = c_dirs_h(d, 2);
-      const int qi = i + di, qj = j + dj, qk = k + dk;
-      const bool inner = qi >= 1 && qj >= 1 && qk >= 1 && qi + qj + qk <= n - 1;
-      if (inner) {
-        const int hq = h + di + 2 * dj + 3 * dk;
-        const int pos = st_ring[(hq & 7) * srl + qk] + qj;
-        X.q[d] = make_double2(__ldcg(ue + pos), __ldg(ke + pos));
-      } else {
-        int off;
-        inc_voff(P, dk + 1, n, qi, qj, qk, off);
-        X.q[d] = make_double2(__ldg(gt + off), __ldg(kt + inc_koff(P, dk + 1, qi, qj)));
-      }
+      const int hq = h + di + 2 * dj + 3 * dk;
+      const int pos = st_ring[(hq & 7) * srl + k + dk] + j + dj;
+      q[d] = make_double2(__ldcg(ue + pos), __ldg(ke + pos));
     }
-    X.k0 = __ldg(ke + e);
-    X.fv = __ldg(fe + e);
-    X.old = __ldcg(ue + e);
-  };
-  auto finish = [&](int e, const Pt &X) {
+    const int self = st_ring[(h & 7) * srl + k] + j;
+    const double old = __ldcg(ue + self), k0 = __ldg(ke + self), fv = __ldg(fe + e);
     double acc = 0.0, diag = 0.0;
     if (VAR == 0) {
 #pragma unroll
       for (int d = 0; d < 14; ++d) {
-        const double sd = dmul(dadd(X.k0, X.q[d].y), coef[d]);
-        acc = dadd(acc, dmul(sd, X.q[d].x));
+        const double sd = dmul(dadd(k0, q[d].y), coef[d]);
+        acc = dadd(acc, dmul(sd, q[d].x));
         diag = dsub(diag, sd);
       }
     } else {
       double b[55];
-      nodal_buffer(X.k0, X.q, b);
-      nodal_gs_terms<0>(acc, diag, X.q, b, sfac);
+      nodal_buffer(k0, q, b);
+      nodal_gs_terms<0>(acc, diag, q, b, sfac);
     }
     if (diag == 0.0) atomicOr(&g_status, 1);
-    __stcg(ue + e, dadd(dmul(dsub(1.0, omega), X.old),
-                        ddiv(dmul(omega, dsub(X.fv, acc)), diag)));
+    const double v = dadd(dmul(dsub(1.0, omega), old), ddiv(dmul(omega, dsub(fv, acc)), diag));
+    __stcg(ue + self, v);
   };
   // the point code of the thread's next point is loaded one point ahead
   // (for the first point of the next hyperplane: before the barrier)
@@ -462,9 +480,7 @@ gs_volume_skew_kernel(GSDesc D, const double *us_c, const double *__restrict__ f
   for (int h = hmin; h <= hmax; ++h) {
     for (int e = ha + first; e < hb; e += stride) {
       const int code_next = e + stride < hb ? __ldg(D.hp_code + e + stride) : 0;
-      Pt a;
-      gather(h, e, code, a);
-      finish(e, a);
+      point(h, e, code);
       code = code_next;
     }
     stage_row(h + 4);

@@ -614,7 +614,10 @@ class Operator:
     def _volume_sweeper(self, du, df, omega):
         """Callable running one volume Gauss-Seidel sweep of every element
         (hyperplane wavefronts; reads the ghost layer, which must be current)
-        on device tensors du, df."""
+        on device tensors du, df.  Between two calls of one sweeper only the
+        surface rows of du (and the ghost layer) may change - the smoothers'
+        surface sweep - and no other sweeper of this operator may run: the
+        hyperplane-major path keeps its copies of f and of du's interior."""
         D = self._device()
         dg = D["grid"]
         st = self._stream()
@@ -640,6 +643,10 @@ class Operator:
         else:
             var, coef = _lib.VAR["scaling"], D["sh"]
         ws = self._skew_workspace()
+        # later sweeps of one sweeper: f's skewed copy and the skewed
+        # interior of u are current (HHG_SKEW_F_CURRENT | HHG_SKEW_U_CURRENT;
+        # between sweeps only surface rows and the ghost shell change)
+        flags = [0]
 
         def volume():
             if ws is None:
@@ -649,8 +656,9 @@ class Operator:
             us, fs, ks = ws
             check(lib.hhg_smooth_volume_skew(dg.ref, var, coef.data_ptr(), float(omega),
                                              du.data_ptr(), df.data_ptr(), us.data_ptr(),
-                                             fs.data_ptr(), ks.data_ptr(), st),
+                                             fs.data_ptr(), ks.data_ptr(), flags[0], st),
                   "smooth_volume_skew")
+            flags[0] = 3
         return volume
 
     def smooth_device(self, du, df, sweeps=1, omega=1.0, check_diag=True):
@@ -685,9 +693,9 @@ class Operator:
 
     def _skew_workspace(self):
         """(us, fs, ks) of the hyperplane-major volume sweep
-        (hhg_smooth_volume_skew): u and f copies per sweep, the skewed
-        coefficient once per operator; None below level 7, where the plain
-        cluster sweep is faster than the two gathers and the scatter)."""
+        (hhg_smooth_volume_skew): u and f copies, the skewed coefficient once
+        per operator; None below level 7, where the plain cluster sweep is
+        faster than the moves in and out."""
         D = self._device()
         if "skew" not in D:
             gt = D["grid"].gt
@@ -696,8 +704,9 @@ class Operator:
                 D["skew"] = None
             else:
                 torch = D["torch"]
-                buf = torch.empty(3 * nv, dtype=torch.float64, device="cuda")
-                us, fs, ks = buf[:nv], buf[nv:2 * nv], buf[2 * nv:]
+                nl = gt.ntets * gt.L      # whole lattices (interior + boundary)
+                buf = torch.empty(2 * nl + nv, dtype=torch.float64, device="cuda")
+                us, ks, fs = buf[:nl], buf[nl:2 * nl], buf[2 * nl:]
                 check(lib.hhg_skew_coefficient(D["grid"].ref, ks.data_ptr(), self._stream()),
                       "skew_coefficient")
                 D["skew"] = (us, fs, ks)

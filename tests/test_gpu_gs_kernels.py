@@ -4,6 +4,8 @@
   the C oracle's lexicographic sweep (kernels.py:510-600) from the GPU's own
   post-surface state, at the automatic CTAs-per-element choice and at forced
   ones (HHG_GS_CLUSTER_N, read once per process -> subprocesses);
+* several sweeps in one call (later sweeps reuse the skewed f and interior)
+  equal the same number of one-sweep calls, bitwise;
 * surface levels: the one-cluster sweep (gs_surface_cluster_kernel, level-
   ordered slots) and the cooperative grid sweep give bitwise equal results.
 """
@@ -92,3 +94,21 @@ def test_surface_cluster_and_grid_sweeps_agree(cuda, tmp_path):
         outs.append(np.load(p))
     assert np.array_equal(outs[0], outs[1])
     assert np.array_equal(outs[0], outs[2])
+
+
+@pytest.mark.parametrize("variant", ["scaling", "nodal"])
+def test_skew_multi_sweep_equals_single_sweeps(cuda, variant):
+    from paper_1709_06793_b200 import Operator, RefinedGrid, sample_nodal
+    from tests.cases import case_mesh, k_c3
+    grid = RefinedGrid(case_mesh("c3"), 7)
+    kf = sample_nodal(k_c3(), grid)
+    op = Operator(grid, variant, kf)
+    assert op._skew_workspace() is not None
+    rng = np.random.default_rng(11)
+    u0 = rng.uniform(-1, 1, grid.n_nodes)
+    f = rng.uniform(-1, 1, grid.n_nodes)
+    a = op.smooth(u0.copy(), f, sweeps=3, omega=0.9)
+    b = u0.copy()
+    for _ in range(3):
+        op.smooth(b, f, sweeps=1, omega=0.9)
+    assert np.array_equal(a, b)

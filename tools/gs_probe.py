@@ -79,14 +79,15 @@ for var in variants:
     h.hhg_ghost_update(dg.ref, u.data_ptr(), st)
     if skew:
         if ws is None:
-            ws = torch.empty(3 * nv, dtype=torch.float64, device="cuda")
-        h.hhg_skew_coefficient(dg.ref, ws[2 * nv:].data_ptr(), st)
+            nl = gt.ntets * gt.L
+            ws = torch.empty(2 * nl + nv, dtype=torch.float64, device="cuda")   # us, ks, fs
+        h.hhg_skew_coefficient(dg.ref, ws[nl:].data_ptr(), st)
 
     def sweep():
         if skew:
             return h.hhg_smooth_volume_skew(dg.ref, 0, sh.data_ptr(), 1.0, u.data_ptr(),
-                                            f.data_ptr(), ws.data_ptr(), ws[nv:].data_ptr(),
-                                            ws[2 * nv:].data_ptr(), st)
+                                            f.data_ptr(), ws.data_ptr(), ws[2 * nl:].data_ptr(),
+                                            ws[nl:].data_ptr(), 0, st)
         return h.hhg_smooth_volume(dg.ref, 0, sh.data_ptr(), 1.0, u.data_ptr(), f.data_ptr(),
                                    st)
     rc = sweep()

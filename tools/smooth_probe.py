@@ -48,7 +48,7 @@ if ws is None:
                                 st))
 else:
     check(lib.hhg_smooth_volume_skew(dg.ref, 0, D["sh"].data_ptr(), 1.0, u.data_ptr(),
-                                     f.data_ptr(), *(x.data_ptr() for x in ws), st))
+                                     f.data_ptr(), *(x.data_ptr() for x in ws), 0, st))
 e2.record()
 torch.cuda.synchronize()
 out = op.apply_device(u)
