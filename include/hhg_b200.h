@@ -341,6 +341,9 @@ typedef struct hhg_surface_gs {
   double *slot_diag;          /* [nslots]                                     */
   int32_t *slot_col;          /* [HHG_SURF_SLOT_PF * nslots]                  */
   double *slot_val;           /* [HHG_SURF_SLOT_PF * nslots]                  */
+  int32_t *slot_dyn;          /* [nslots] bit m: entry m is a row of the
+                                 previous level (read after the barrier; the
+                                 others are prefetched across it)            */
 } hhg_surface_gs;
 #define HHG_SURF_SLOT_PF 24
 
@@ -387,12 +390,15 @@ int hhg_ipc_close_handle(void *ptr);
 int hhg_smooth_surface_prepare(const hhg_grid *g, const hhg_surface *s,
                                const hhg_surface_gs *gs, void *stream);
 /* fill gs->slot_* (allocated by the caller) from the level schedule and
- * the prepared rows; call after _prepare and whenever they change */
+ * the prepared rows; call after _prepare and whenever they change.
+ * gid_level[x] (device, nlv entries): level of the schedule row with global
+ * id x, -1 for ids that are not rows of the sweep */
 int hhg_smooth_surface_slots(const hhg_grid *g, const hhg_surface *s,
-                             const hhg_surface_gs *gs, void *stream);
+                             const hhg_surface_gs *gs, const int32_t *gid_level,
+                             int64_t nlv, void *stream);
 /* every level of the surface sweep in one launch: one thread-block cluster
- * with a cluster barrier between levels when gs->slot_gid is set, else a
- * cooperative grid with grid barriers */
+ * with a cluster barrier between levels (narrow schedules, slots built), or
+ * a cooperative grid with grid barriers */
 int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s,
                            const hhg_surface_gs *gs, double omega, double *u,
                            const double *f, void *stream);

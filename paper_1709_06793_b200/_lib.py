@@ -77,7 +77,7 @@ class HhgSurfaceGS(ctypes.Structure):
     _fields_ = [("level_rows", vp), ("level_ptr", vp), ("nlev", ctypes.c_int64),
                 ("ent_ptr", vp), ("ent_col", vp), ("ent_val", vp), ("row_diag", vp),
                 ("nslots", ctypes.c_int64), ("slot_gid", vp), ("slot_cnt", vp),
-                ("slot_diag", vp), ("slot_col", vp), ("slot_val", vp)]
+                ("slot_diag", vp), ("slot_col", vp), ("slot_val", vp), ("slot_dyn", vp)]
 
 
 SURF_SLOT_PF = 24   # HHG_SURF_SLOT_PF
@@ -122,7 +122,8 @@ EXPORTS = {
                                              vp, vp, vp, vp]),
     "hhg_smooth_surface_slots": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
                                                 ctypes.POINTER(HhgSurface),
-                                                ctypes.POINTER(HhgSurfaceGS), vp]),
+                                                ctypes.POINTER(HhgSurfaceGS), vp,
+                                                ctypes.c_int64, vp]),
     "hhg_smooth_surface_all": (ctypes.c_int, [ctypes.POINTER(HhgGrid),
                                               ctypes.POINTER(HhgSurface),
                                               ctypes.POINTER(HhgSurfaceGS), ctypes.c_double,

@@ -918,19 +918,20 @@ static SurfGSDesc surf_gs_desc(const hhg_grid *g, const hhg_surface *s, const hh
   G.slot_col = gs->slot_col;
   G.slot_diag = gs->slot_diag;
   G.slot_val = gs->slot_val;
+  G.slot_dyn = gs->slot_dyn;
   return G;
 }
 
 int hhg_smooth_surface_slots(const hhg_grid *g, const hhg_surface *s, const hhg_surface_gs *gs,
-                             void *stream) {
+                             const int32_t *gid_level, int64_t nlv, void *stream) {
   if (gs->nslots <= 0) return HHG_OK;
   if (!gs->slot_gid || !gs->slot_cnt || !gs->slot_diag || !gs->slot_col || !gs->slot_val ||
-      !gs->level_rows)
+      !gs->slot_dyn || !gs->level_rows || !gid_level)
     return HHG_ERR_ARG;
   SurfGSDesc G = surf_gs_desc(g, s, gs, 1.0, nullptr, nullptr);
   surface_slots_kernel<<<(int)((gs->nslots + 255) / 256), 256, 0, S(stream)>>>(
       G, reinterpret_cast<long long *>(gs->slot_gid), gs->slot_cnt, gs->slot_diag, gs->slot_col,
-      gs->slot_val);
+      gs->slot_val, gs->slot_dyn, gid_level, nlv);
   return check("surface_slots_kernel");
 }
 
@@ -985,7 +986,7 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_su
     return e ? atoi(e) : -1;
   }();
   const long long mean_width = (s->nrows + gs->nlev - 1) / gs->nlev;
-  const int ncl = env_cl >= 0 ? env_cl : (mean_width <= 1024 ? 16 : 0);
+  const int ncl = env_cl >= 0 ? env_cl : (mean_width <= 1024 ? 16 : 0);   // -1: auto
   if (ncl > 0 && gs->slot_gid && gs->nslots == s->nrows) {
     if (ncl > 8)
       cudaFuncSetAttribute(gs_surface_cluster_kernel,

@@ -508,7 +508,7 @@ struct SurfGSDesc {
   // level-ordered slots (gs_surface_cluster_kernel)
   long long nslots;
   const long long *slot_gid;
-  const int *slot_cnt, *slot_col;
+  const int *slot_cnt, *slot_col, *slot_dyn;
   const double *slot_diag, *slot_val;
 };
 
@@ -959,48 +959,52 @@ gs_surface_all_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
 // The same sweep on ONE thread-block cluster, from the level-ordered slots
 // (hhg_surface_gs.slot_*): a level's rows are spread over the cluster's
 // CTAs; between levels a split hardware cluster barrier (arrive.release,
-// then wait.acquire; cluster scope) replaces the grid barrier, and the
-// static part of each thread's next row (id, count, diagonal, f, column
-// ids: one coalesced load per field, no dependent address chain) is fetched
-// between the arrive and the wait, so it overlaps the barrier.  After the
-// wait one round of loads remains on the level's critical path: the
-// neighbour values (through L2: other CTAs write them) and the weights.
-// Entries, order and arithmetic are gs_surface_row_csr's: bitwise the same.
+// then wait.acquire; cluster scope) replaces the grid barrier.  Between the
+// arrive and the wait each thread fetches its next row - id, count,
+// diagonal, f, column ids, weights (one coalesced load per field) - AND the
+// neighbour values that cannot change before that row runs: volume and
+// Dirichlet ids, rows of earlier levels (final since the last wait) and of
+// later levels (still old).  Only neighbours in the level just written
+// (slot_dyn bits, ~2 per row) are read after the wait.  Entries, order and
+// arithmetic are gs_surface_row_csr's: bitwise the same.
 constexpr int kSlotPF = HHG_SURF_SLOT_PF;
 struct SlotRow {
   long long gid;
   int cnt;
+  unsigned dyn;
   double diag, fv;
   int col[kSlotPF];
+  double w[kSlotPF], x[kSlotPF];
 };
 
 __device__ __forceinline__ void slot_prefetch(const SurfGSDesc &G, long long e, SlotRow &p) {
   const long long ns = G.nslots;
+  const double *u = G.s.u;
   p.gid = __ldg(G.slot_gid + e);
   p.cnt = __ldg(G.slot_cnt + e);
+  p.dyn = (unsigned)__ldg(G.slot_dyn + e);
   p.diag = __ldg(G.slot_diag + e);
 #pragma unroll
-  for (int m = 0; m < kSlotPF; ++m)      // padded slots hold column 0
+  for (int m = 0; m < kSlotPF; ++m) {   // padded slots hold (0, 0.0)
     p.col[m] = __ldg(G.slot_col + m * ns + e);
+    p.w[m] = __ldg(G.slot_val + m * ns + e);
+  }
   p.fv = __ldg(G.s.f + p.gid);
-}
-
-__device__ __forceinline__ void slot_finish(const SurfGSDesc &G, long long e, const SlotRow &p) {
-  double *u = const_cast<double *>(G.s.u);
-  // weights (static, independent) in the same round as the neighbours
-  const long long ns = G.nslots;
-  double x[kSlotPF], w[kSlotPF];
 #pragma unroll
   for (int m = 0; m < kSlotPF; ++m)
-    if (m < p.cnt) {
-      x[m] = __ldcg(u + (unsigned)p.col[m]);
-      w[m] = __ldg(G.slot_val + m * ns + e);
-    }
+    if (m < p.cnt && !(p.dyn >> m & 1)) p.x[m] = __ldcg(u + (unsigned)p.col[m]);
+}
+
+__device__ __forceinline__ void slot_finish(const SurfGSDesc &G, long long e, SlotRow &p) {
+  double *u = const_cast<double *>(G.s.u);
+#pragma unroll
+  for (int m = 0; m < kSlotPF; ++m)
+    if (m < p.cnt && (p.dyn >> m & 1)) p.x[m] = __ldcg(u + (unsigned)p.col[m]);
   const double old = __ldcg(u + p.gid);
   double acc = 0.0;
 #pragma unroll
   for (int m = 0; m < kSlotPF; ++m)
-    if (m < p.cnt) acc = dadd(acc, dmul(w[m], x[m]));
+    if (m < p.cnt) acc = dadd(acc, dmul(p.w[m], p.x[m]));
   if (p.cnt > kSlotPF) {               // long (edge / vertex) rows: the rest
     const long long r = __ldg(G.level_rows + e);
     const long long e1 = __ldg(G.ent_ptr + r + 1);
@@ -1028,19 +1032,26 @@ __device__ __forceinline__ void slot_finish(const SurfGSDesc &G, long long e, co
 }
 
 __global__ void surface_slots_kernel(SurfGSDesc G, long long *gid, int *cnt, double *diag,
-                                     int *col, double *val) {
+                                     int *col, double *val, int *dyn, const int *gid_level,
+                                     long long nlv) {
   const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long ns = G.nslots;
   if (e >= ns) return;
   const long long r = G.level_rows[e];
   const long long e0 = G.ent_ptr[r], c = G.ent_ptr[r + 1] - e0;
-  gid[e] = G.s.rows[r];
+  const long long g = G.s.rows[r];
+  const int lv = g < nlv ? gid_level[g] : -1;
+  gid[e] = g;
   cnt[e] = (int)c;
   diag[e] = G.row_diag[r];
+  unsigned bits = 0;
   for (int m = 0; m < kSlotPF; ++m) {
-    col[m * ns + e] = m < c ? G.ent_col[e0 + m] : 0;
+    const int cl = m < c ? G.ent_col[e0 + m] : 0;
+    col[m * ns + e] = cl;
     val[m * ns + e] = m < c ? G.ent_val[e0 + m] : 0.0;
+    if (m < c && cl < nlv && gid_level[cl] == lv - 1 && lv > 0) bits |= 1u << m;
   }
+  dyn[e] = (int)bits;
 }
 
 #ifndef HHG_SURF_CT

@@ -536,13 +536,22 @@ class DeviceSurface:
                      torch.empty(max(ns, 1), dtype=torch.float64, device="cuda"),
                      torch.empty(max(ns, 1) * SURF_SLOT_PF, dtype=torch.int32, device="cuda"),
                      torch.empty(max(ns, 1) * SURF_SLOT_PF, dtype=torch.float64,
-                                 device="cuda")]
+                                 device="cuda"),
+                     torch.empty(max(ns, 1), dtype=torch.int32, device="cuda")]
             d.nslots = ns
-            (d.slot_gid, d.slot_cnt, d.slot_diag, d.slot_col,
-             d.slot_val) = (x.data_ptr() for x in slots)
-            check(lib.hhg_smooth_surface_slots(dg.ref, self.ref, c["ref"],
+            (d.slot_gid, d.slot_cnt, d.slot_diag, d.slot_col, d.slot_val,
+             d.slot_dyn) = (x.data_ptr() for x in slots)
+            # level of every schedule row by global id (entries of the
+            # previous level are the ones read after the barrier)
+            rows = np.asarray(self.st.rows, dtype=np.int64)
+            lv = np.full(int(rows.max()) + 1 if len(rows) else 1, -1, dtype=np.int32)
+            lv[rows[order]] = np.repeat(np.arange(nlev, dtype=np.int32), np.diff(ptr))
+            lv_d = torch.as_tensor(lv, device="cuda")
+            check(lib.hhg_smooth_surface_slots(dg.ref, self.ref, c["ref"], lv_d.data_ptr(),
+                                               len(lv),
                                                torch.cuda.current_stream().cuda_stream),
                   "smooth_surface_slots")
+            torch.cuda.current_stream().synchronize()   # lv_d is temporary
             c["keep"] += keep + slots
             self._levels = nlev
         return {"ref": c["ref"], "nlev": self._levels}

@@ -6,8 +6,9 @@
   ones (HHG_GS_CLUSTER_N, read once per process -> subprocesses);
 * several sweeps in one call (later sweeps reuse the skewed f and interior)
   equal the same number of one-sweep calls, bitwise;
-* surface levels: the one-cluster sweep (gs_surface_cluster_kernel, level-
-  ordered slots) and the cooperative grid sweep give bitwise equal results.
+* surface rows: the one-cluster level sweep (gs_surface_cluster_kernel,
+  level-ordered slots) and the cooperative grid level sweep give bitwise
+  equal results.
 """
 import os
 import subprocess
@@ -85,15 +86,16 @@ def test_skew_volume_sweep_cluster_sizes(cuda, ctas):
          "check_skew_volume('scaling', 0.9)", HHG_GS_CLUSTER_N=ctas)
 
 
-def test_surface_cluster_and_grid_sweeps_agree(cuda, tmp_path):
+def test_surface_sweep_forms_agree(cuda, tmp_path):
+    # automatic choice, one cluster of 8 / 16 CTAs, cooperative grid
     outs = []
-    for mode in ("0", "8", "16"):
-        p = str(tmp_path / f"u{mode}.npy")
+    for cl in ("-1", "0", "8", "16"):
+        p = str(tmp_path / f"u{cl}.npy")
         _sub(f"from tests.test_gpu_gs_kernels import smooth_c3; smooth_c3({p!r})",
-             HHG_SURF_CLUSTER=mode)
+             HHG_SURF_CLUSTER=cl)
         outs.append(np.load(p))
-    assert np.array_equal(outs[0], outs[1])
-    assert np.array_equal(outs[0], outs[2])
+    for o in outs[1:]:
+        assert np.array_equal(outs[0], o)
 
 
 @pytest.mark.parametrize("variant", ["scaling", "nodal"])
