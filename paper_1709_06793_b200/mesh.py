@@ -52,6 +52,10 @@ DIRS_3D = np.array(
      (-1, 0, 0), (0, -1, 0), (0, 0, -1), (-1, 1, 0), (-1, 0, 1), (0, -1, 1),
      (-1, 1, -1)], dtype=np.int64)
 
+# The six directions of a 2-D (triangle) lattice node, mirrored the same way
+# (`mesh.py:41-43`); used by the 2-D MA2 set-up (ma2.py) and kernels.
+DIRS_2D = np.array([(1, 0), (0, 1), (1, -1), (-1, 0), (0, -1), (-1, 1)], dtype=np.int64)
+
 LOCAL_EDGES_3D = ((0, 1), (0, 2), (0, 3), (1, 2), (1, 3), (2, 3))
 # face f is opposite local vertex f
 LOCAL_FACES_3D = ((1, 2, 3), (0, 2, 3), (0, 1, 3), (0, 1, 2))

@@ -420,9 +420,54 @@ def sec_coeff():
     save("coeff", **out)
 
 
+def sec_ma2_marks():
+    """The reference's 2-D scaling_ma2 set-up (operators.ma2_marks and the
+    Operator's per-element selector inputs) on its two obtuse 2-D meshes
+    with its 2-D catalog coefficients, plus the element kernels on those
+    inputs (seeded element lattices)."""
+    from hhgscale.coefficients import catalog
+    from hhgscale.operators import ma2_marks as r_marks
+    out = {}
+    rng = np.random.default_rng(31)
+    cases = [("square_sig", RM.obtuse_square(), 4, catalog("sigmoid2d")),
+             ("square_sin", RM.obtuse_square(), 3, catalog("sin2d")),
+             ("kite_sig", RM.obtuse_kite_band(), 4, catalog("sigmoid2d")),
+             ("kite_sig5", RM.obtuse_kite_band(), 5, catalog("sigmoid2d"))]
+    for tag, mesh, lvl, fn in cases:
+        g = RM.RefinedGrid(mesh, lvl)
+        kf = r_sample(fn, g)
+        marked, gray, km = r_marks(g, kf)
+        op = ROperator(g, "scaling_ma2", kf)
+        assert np.array_equal(op.ma2_marked, marked)
+        n = g.n
+        L = (n + 1) * (n + 2) // 2
+        ni = (n - 1) * (n - 2) // 2
+        ne = mesh.n_elements
+        u = rng.uniform(-1, 1, (ne, L))
+        f = rng.uniform(-1, 1, (ne, ni))
+        app = np.empty((ne, ni))
+        gs = np.empty((ne, L))
+        for t in range(ne):
+            kn.apply_scaling_2d(n, g.lat.base, u[t], kf.values[t], op._kg[t], op._gmask[t],
+                                op._sh[t], app[t])
+            w = u[t].copy()
+            kn.gs_scaling_2d(n, g.lat.base, w, f[t], kf.values[t], op._kg[t], op._gmask[t],
+                             op._sh[t], 0.9)
+            gs[t] = w
+        out.update({f"{tag}_verts": mesh.vertices, f"{tag}_elems": mesh.elements,
+                    f"{tag}_level": np.int64(lvl), f"{tag}_values": kf.values,
+                    f"{tag}_marked": marked, f"{tag}_gray": gray, f"{tag}_kmin": km.values,
+                    f"{tag}_sh": np.stack(op._sh), f"{tag}_kg": np.stack(op._kg),
+                    f"{tag}_g": op._gmask, f"{tag}_u": u, f"{tag}_f": f,
+                    f"{tag}_apply": app, f"{tag}_gs09": gs})
+        print(f"  {tag}: marked {marked.tolist()} gray {gray.tolist()}")
+    save("ma2_marks", **out)
+
+
 SECTIONS = {"mesh": sec_mesh, "kernels": sec_kernels, "applies": sec_applies,
             "c3": sec_c3_checksums, "c2": sec_c2_cg, "mg": sec_mg_small, "c4": sec_c4_mg,
-            "tensor": sec_tensor, "coeff": sec_coeff, "norms": sec_norms, "ma2_2d": sec_ma2_2d}
+            "tensor": sec_tensor, "coeff": sec_coeff, "norms": sec_norms, "ma2_2d": sec_ma2_2d,
+            "ma2_marks": sec_ma2_marks}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(SECTIONS)):
