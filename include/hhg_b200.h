@@ -344,6 +344,9 @@ typedef struct hhg_surface_gs {
   int32_t *slot_dyn;          /* [nslots] bit m: entry m is a row of the
                                  previous level (read after the barrier; the
                                  others are prefetched across it)            */
+  uint32_t *sweep_bar;        /* [1] scratch: arrival counter of the grid
+                                 sweep's barrier (one per schedule, so
+                                 sweeps on different streams never share) */
 } hhg_surface_gs;
 #define HHG_SURF_SLOT_PF 24
 

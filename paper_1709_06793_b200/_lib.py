@@ -77,7 +77,8 @@ class HhgSurfaceGS(ctypes.Structure):
     _fields_ = [("level_rows", vp), ("level_ptr", vp), ("nlev", ctypes.c_int64),
                 ("ent_ptr", vp), ("ent_col", vp), ("ent_val", vp), ("row_diag", vp),
                 ("nslots", ctypes.c_int64), ("slot_gid", vp), ("slot_cnt", vp),
-                ("slot_diag", vp), ("slot_col", vp), ("slot_val", vp), ("slot_dyn", vp)]
+                ("slot_diag", vp), ("slot_col", vp), ("slot_val", vp), ("slot_dyn", vp),
+                ("sweep_bar", vp)]
 
 
 SURF_SLOT_PF = 24   # HHG_SURF_SLOT_PF

@@ -975,21 +975,29 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_su
   SurfGSDesc G = surf_gs_desc(g, s, gs, omega, u, f);
   const long long *lp = reinterpret_cast<const long long *>(gs->level_ptr);
   int nl = (int)gs->nlev;
-  // narrow sweeps (mean level width <= 1024 rows: level 6, 7 grids): one
+  // narrow sweeps (mean level width <= 512 rows: level 6 grids): one
   // 16-CTA thread-block cluster walks the levels, a cluster barrier between
-  // them (measured 8% faster than the grid barrier there); wider sweeps
-  // need the memory parallelism of the whole GPU: the cooperative grid.
-  // HHG_SURF_CLUSTER overrides: CTAs per cluster (> 8 needs the
-  // non-portable opt-in), 0 = always the cooperative grid.
+  // them; wider sweeps need the memory parallelism of many SMs: a
+  // cooperative grid with a split software barrier.  Both from the
+  // level-ordered slots, prefetching each thread's next row across the
+  // barrier.  HHG_SURF_CLUSTER overrides: CTAs per cluster (> 8 needs the
+  // non-portable opt-in), 0 = grid; HHG_SURF_LEGACY=1: the round-1 grid
+  // kernel (cooperative groups grid.sync, no slots).
   static const int env_cl = [] {
     const char *e = getenv("HHG_SURF_CLUSTER");
     return e ? atoi(e) : -1;
   }();
+  static const bool legacy = [] {
+    const char *e = getenv("HHG_SURF_LEGACY");
+    return e && atoi(e) != 0;
+  }();
   const long long mean_width = (s->nrows + gs->nlev - 1) / gs->nlev;
-  const int ncl = env_cl >= 0 ? env_cl : (mean_width <= 1024 ? 16 : 0);   // -1: auto
-  if (ncl > 0 && gs->slot_gid && gs->nslots == s->nrows) {
+  const int ncl = env_cl >= 0 ? env_cl : (mean_width <= 512 ? 16 : 0);   // -1: auto
+  const bool slots = gs->slot_gid && gs->slot_dyn && gs->sweep_bar && gs->nslots == s->nrows &&
+                     !legacy;
+  if (slots && ncl > 0) {
     if (ncl > 8)
-      cudaFuncSetAttribute(gs_surface_cluster_kernel,
+      cudaFuncSetAttribute(gs_surface_slots_kernel<false>,
                            cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncl);
@@ -1003,9 +1011,29 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_su
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gs_surface_cluster_kernel, G, lp, nl);
+    unsigned *nobar = nullptr;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gs_surface_slots_kernel<false>, G, lp, nl, nobar);
     if (e != cudaSuccess) {
-      fprintf(stderr, "hhg_b200: gs_surface_cluster_kernel: %s\n", cudaGetErrorString(e));
+      fprintf(stderr, "hhg_b200: gs_surface_slots_kernel: %s\n", cudaGetErrorString(e));
+      return HHG_ERR_CUDA;
+    }
+    return HHG_OK;
+  }
+  if (slots) {
+    static std::map<int, int> gcaps;
+    const int cap = device_capacity(gs_surface_slots_kernel<true>, HHG_SURF_GRID_CT, gcaps);
+    int blocks = (int)std::min<long long>((mean_width + 7) / 8, cap);
+    if (blocks < 8) blocks = std::min(8, cap);
+    unsigned *bar = gs->sweep_bar;
+    cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), S(stream));
+    if (e == cudaSuccess) {
+      void *args[] = {(void *)&G, (void *)&lp, (void *)&nl, (void *)&bar};
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      e = cudaLaunchCooperativeKernel((void *)gs_surface_slots_kernel<true>, blocks,
+                                      HHG_SURF_GRID_CT, args, 0, S(stream));
+    }
+    if (e != cudaSuccess) {
+      fprintf(stderr, "hhg_b200: gs_surface_slots_kernel<grid>: %s\n", cudaGetErrorString(e));
       return HHG_ERR_CUDA;
     }
     return HHG_OK;

@@ -505,7 +505,7 @@ struct SurfGSDesc {
   const long long *ent_ptr;
   int *ent_col;
   double *ent_val, *row_diag;
-  // level-ordered slots (gs_surface_cluster_kernel)
+  // level-ordered slots (gs_surface_slots_kernel)
   long long nslots;
   const long long *slot_gid;
   const int *slot_cnt, *slot_col, *slot_dyn;
@@ -1057,10 +1057,22 @@ __global__ void surface_slots_kernel(SurfGSDesc G, long long *gid, int *cnt, dou
 #ifndef HHG_SURF_CT
 #define HHG_SURF_CT 256          // threads per CTA of the cluster surface sweep
 #endif
-__global__ void __launch_bounds__(HHG_SURF_CT)
-gs_surface_cluster_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
-  const long long nb = cluster_nctas();
-  const long long tid = threadIdx.x * nb + cluster_ctarank();
+#ifndef HHG_SURF_GRID_CT
+#define HHG_SURF_GRID_CT 64      // threads per CTA of the grid surface sweep
+#endif
+
+// GRID = false: one thread-block cluster, hardware split barrier.
+// GRID = true: a cooperative grid (wide schedules need more SMs' memory
+// parallelism) with a split software barrier: arrive = block barrier, then
+// one thread's fence + atomic add on *bar; wait = that thread's acquire
+// spin until all blocks of this level arrived, then a block barrier.
+// Either way the next row's static part is fetched between arrive and wait.
+template <bool GRID>
+__global__ void __launch_bounds__(GRID ? HHG_SURF_GRID_CT : HHG_SURF_CT)
+gs_surface_slots_kernel(SurfGSDesc G, const long long *level_ptr, int nlev, unsigned *bar) {
+  const long long nb = GRID ? (long long)gridDim.x : (long long)cluster_nctas();
+  const long long rank = GRID ? (long long)blockIdx.x : (long long)cluster_ctarank();
+  const long long tid = threadIdx.x * nb + rank;
   const long long nth = nb * blockDim.x;
   SlotRow pf;
   bool have = nlev > 0 && level_ptr[0] + tid < level_ptr[1];
@@ -1073,14 +1085,33 @@ gs_surface_cluster_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
       have = false;
       slot_finish(G, e, pf);
     }
-    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    if constexpr (GRID) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+      }
+    } else {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    }
     have = false;
     if (lv + 1 < nlev) {
       const long long e = b + tid;
       have = e < level_ptr[lv + 2];
       if (have) slot_prefetch(G, e, pf);
     }
-    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if constexpr (GRID) {
+      if (threadIdx.x == 0) {
+        const unsigned target = (unsigned)((lv + 1) * nb);
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+      }
+      __syncthreads();
+    } else {
+      asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    }
   }
 }
 

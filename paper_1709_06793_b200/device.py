@@ -537,10 +537,11 @@ class DeviceSurface:
                      torch.empty(max(ns, 1) * SURF_SLOT_PF, dtype=torch.int32, device="cuda"),
                      torch.empty(max(ns, 1) * SURF_SLOT_PF, dtype=torch.float64,
                                  device="cuda"),
-                     torch.empty(max(ns, 1), dtype=torch.int32, device="cuda")]
+                     torch.empty(max(ns, 1), dtype=torch.int32, device="cuda"),
+                     torch.zeros(1, dtype=torch.int32, device="cuda")]
             d.nslots = ns
-            (d.slot_gid, d.slot_cnt, d.slot_diag, d.slot_col, d.slot_val,
-             d.slot_dyn) = (x.data_ptr() for x in slots)
+            (d.slot_gid, d.slot_cnt, d.slot_diag, d.slot_col, d.slot_val, d.slot_dyn,
+             d.sweep_bar) = (x.data_ptr() for x in slots)
             # level of every schedule row by global id (entries of the
             # previous level are the ones read after the barrier)
             rows = np.asarray(self.st.rows, dtype=np.int64)

@@ -6,9 +6,9 @@
   ones (HHG_GS_CLUSTER_N, read once per process -> subprocesses);
 * several sweeps in one call (later sweeps reuse the skewed f and interior)
   equal the same number of one-sweep calls, bitwise;
-* surface rows: the one-cluster level sweep (gs_surface_cluster_kernel,
-  level-ordered slots) and the cooperative grid level sweep give bitwise
-  equal results.
+* surface rows: the level sweep from the level-ordered slots on one
+  cluster or on a cooperative grid (gs_surface_slots_kernel) and the
+  round-1 grid kernel give bitwise equal results.
 """
 import os
 import subprocess
@@ -87,12 +87,12 @@ def test_skew_volume_sweep_cluster_sizes(cuda, ctas):
 
 
 def test_surface_sweep_forms_agree(cuda, tmp_path):
-    # automatic choice, one cluster of 8 / 16 CTAs, cooperative grid
+    # automatic choice, one cluster of 8 / 16 CTAs, grid, round-1 grid kernel
     outs = []
-    for cl in ("-1", "0", "8", "16"):
-        p = str(tmp_path / f"u{cl}.npy")
+    for cl, legacy in (("-1", "0"), ("0", "0"), ("8", "0"), ("16", "0"), ("0", "1")):
+        p = str(tmp_path / f"u{cl}{legacy}.npy")
         _sub(f"from tests.test_gpu_gs_kernels import smooth_c3; smooth_c3({p!r})",
-             HHG_SURF_CLUSTER=cl)
+             HHG_SURF_CLUSTER=cl, HHG_SURF_LEGACY=legacy)
         outs.append(np.load(p))
     for o in outs[1:]:
         assert np.array_equal(outs[0], o)
