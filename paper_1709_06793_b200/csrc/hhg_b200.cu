@@ -359,6 +359,10 @@ static int device_capacity(K kern, int threads, std::map<int, int> &cache) {
 #define HHG_GS_CLUSTER 4         // CTAs per element of the cluster sweeps (0: off)
 #endif
 
+#ifndef HHG_GS_CLUSTER_MAX
+#define HHG_GS_CLUSTER_MAX 16    // most CTAs per element of the hyperplane-major sweep
+#endif
+
 // CTAs per element of the cluster volume sweeps (HHG_GS_CLUSTER_N overrides;
 // > 8 needs the non-portable opt-in)
 static int gs_cluster() {
@@ -1141,7 +1145,7 @@ int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef, d
     skew_f_kernel<<<dim3((int)((g->nvol + 255) / 256), g->ntets), 256, 0, S(stream)>>>(G, f, fs);
     if ((rc = check("skew_f_kernel"))) return rc;
   }
-  // CTAs per element: the most (<= 8) with which every element's cluster is
+  // CTAs per element: the most (<= 16) with which every element's cluster is
   // co-resident in one wave (the sweep is latency-bound: more threads per
   // hyperplane help, a second wave of elements does not); at least 4.
   // HHG_GS_CLUSTER_N fixes it.
@@ -1166,7 +1170,8 @@ int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef, d
     auto it = pick.find(key);
     if (it == pick.end()) {
       int best = 4;
-      for (int c = 8; c > 4; --c) {
+      cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      for (int c = HHG_GS_CLUSTER_MAX; c > 4; --c) {
         cfg.gridDim = dim3(G.ntets * c);
         attr[0].val.clusterDim.x = c;
         int fit = 0;
