@@ -327,6 +327,49 @@ def sec_c4_mg():
          u_norm=np.linalg.norm(u))
 
 
+def sec_pcg():
+    """Multigrid-preconditioned CG (BASELINE config 4 names it; the
+    reference has none): the flexible-beta PCG of our `multigrid.pcg`,
+    written here in numpy on the REFERENCE's Operator (apply / residual) and
+    `vcycle` (V(2,2) from a zero guess as the preconditioner), so the
+    residual history pins our device PCG against the reference's pieces."""
+    from hhgscale.multigrid import vcycle as r_vcycle
+    lvl = 5
+    hier = GridHierarchy(rmesh(case_mesh("c3")), lvl, "scaling", c4_field())
+    g = hier.grids[lvl]
+    op = hier.ops[lvl]
+    rng = np.random.default_rng(4)
+    f = rng.normal(size=g.n_nodes)
+    f[g.dirichlet_mask] = 0.0
+    hscale = 2.0 ** (-lvl * 3 / 2.0)
+    x = np.zeros(g.n_nodes)
+    r = op.residual(x, f)
+    res = [hscale * float(np.linalg.norm(r))]
+    target = 1e-8 * res[0]
+
+    def precond(rr):
+        return r_vcycle(hier, np.zeros(g.n_nodes), rr, None, 2, 2)
+
+    z = precond(r)
+    p = z.copy()
+    rz = float(r @ z)
+    for _ in range(200):
+        Ap = op.apply(p)
+        alpha = rz / float(p @ Ap)
+        x = x + alpha * p
+        r_new = r - alpha * Ap
+        res.append(hscale * float(np.linalg.norm(r_new)))
+        if res[-1] <= target:
+            break
+        z = precond(r_new)
+        beta = float((r_new - r) @ z) / rz
+        p = z + beta * p
+        rz = float(r_new @ z)
+        r = r_new
+    print(f"  pcg: {len(res) - 1} iterations, residuals {res[0]:.3e} -> {res[-1]:.3e}")
+    save("pcg_c4", residuals=np.array(res), iterations=len(res) - 1, u_sample=x[::101])
+
+
 def sec_tensor():
     """Tensor-coefficient (M = 6) pins: the reference's tensor numba kernels
     on seeded lattices, tensor Operators (tensor3d_poly on the unit cube,
@@ -467,7 +510,7 @@ def sec_ma2_marks():
 SECTIONS = {"mesh": sec_mesh, "kernels": sec_kernels, "applies": sec_applies,
             "c3": sec_c3_checksums, "c2": sec_c2_cg, "mg": sec_mg_small, "c4": sec_c4_mg,
             "tensor": sec_tensor, "coeff": sec_coeff, "norms": sec_norms, "ma2_2d": sec_ma2_2d,
-            "ma2_marks": sec_ma2_marks}
+            "ma2_marks": sec_ma2_marks, "pcg": sec_pcg}
 
 if __name__ == "__main__":
     for name in (sys.argv[1:] or list(SECTIONS)):

@@ -143,6 +143,24 @@ def test_mg_preconditioned_cg_config4_like(cuda):
     assert rep.residuals[-1] <= 1e-8 * rep.residuals[0]
 
 
+def test_pcg_matches_reference_components(cuda):
+    """PCG pinned against the same flexible-beta PCG written in numpy on the
+    REFERENCE's Operator and vcycle (tests/golden/make_golden.py sec_pcg,
+    config-4 mesh and field at L5): same iteration count, residual history
+    within rtol 1e-6, solution samples within 1e-7."""
+    from paper_1709_06793_b200.multigrid import pcg
+    g = golden("pcg_c4")
+    lvl = 5
+    hier = GridHierarchy(case_mesh("c3"), lvl, "scaling", c4_field())
+    grid = hier.grids[lvl]
+    f = np.random.default_rng(4).normal(size=grid.n_nodes)
+    f[grid.dirichlet_mask] = 0.0
+    u, rep = pcg(hier, f, stop="drop:1e-8", pre=2, post=2)
+    assert rep.iterations == int(g["iterations"])
+    assert np.allclose(rep.residuals, g["residuals"], rtol=1e-6, atol=0)
+    assert np.abs(u[::101] - g["u_sample"]).max() <= 1e-7 * np.abs(u).max()
+
+
 @pytest.mark.parametrize("variant", ["scaling", "nodal"])
 def test_vcycle_fixed_point(cuda, variant):
     """The discrete solution is a fixed point of the V-cycle (the reference's
