@@ -190,7 +190,14 @@ def run_own(args):
     if imap is not None:
         from paper_1709_06793_b200.shard import ShardedOperator
         idx_t = {k: torch.as_tensor(v, device="cuda") for k, v in imap.neighbours.items()}
-        sop = ShardedOperator(op, imap, dist, grid.dirichlet_mask, transport=args.exchange)
+        from paper_1709_06793_b200.shard import PeerUnavailable
+        try:
+            sop = ShardedOperator(op, imap, dist, grid.dirichlet_mask, transport=args.exchange)
+        except PeerUnavailable as exc:     # agreed on every rank: fall back to NCCL
+            if rank == 0:
+                print(f"bench: p2p exchange unavailable ({exc}); using nccl", file=sys.stderr)
+            args.exchange = "nccl"
+            sop = ShardedOperator(op, imap, dist, grid.dirichlet_mask, transport="nccl")
     torch.cuda.synchronize()
     t_setup = time.time() - t_setup
 

@@ -111,6 +111,10 @@ def exchange_partials(out, imap: InterfaceMap, dist, index_tensors=None):
     return out
 
 
+class PeerUnavailable(RuntimeError):
+    """CUDA IPC peer mapping failed on some rank (raised on all ranks)."""
+
+
 class PeerExchange:
     """Interface exchange over peer memory (NVLink / NVSwitch, CUDA IPC):
     the compute step and the transfer in one kernel.
@@ -192,24 +196,42 @@ class PeerExchange:
     # -- connection --------------------------------------------------------
     def connect(self, dist):
         """Exchange CUDA IPC handles of the receive buffers and counters with
-        the neighbours (all ranks call this collectively)."""
+        the neighbours (all ranks call this collectively).  A failure on any
+        rank - getting or opening a handle - raises PeerUnavailable on EVERY
+        rank (the outcome is agreed through the same collectives), so callers
+        can fall back to another transport without a hang."""
         import ctypes
         from ._lib import check, lib
-        mine = {}
-        for nb in self.nbrs:
-            hr, hf = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
-            check(lib.hhg_ipc_get_handle(self.recv[nb], hr), "ipc_get_handle")
-            check(lib.hhg_ipc_get_handle(self.flag[nb], hf), "ipc_get_handle")
-            mine[nb] = (hr.raw, hf.raw)
+        mine, err = {}, None
+        try:
+            for nb in self.nbrs:
+                hr, hf = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
+                check(lib.hhg_ipc_get_handle(self.recv[nb], hr), "ipc_get_handle")
+                check(lib.hhg_ipc_get_handle(self.flag[nb], hf), "ipc_get_handle")
+                mine[nb] = (hr.raw, hf.raw)
+        except Exception as exc:                  # noqa: BLE001 - reported to every rank
+            err = f"rank {self.rank}: {exc}"
         allh = [None] * dist.get_world_size()
-        dist.all_gather_object(allh, mine)
-        for nb in self.nbrs:
-            hr, hf = allh[nb][self.rank]                # nb's buffers that receive from me
-            pr, pf = ctypes.c_void_p(), ctypes.c_void_p()
-            check(lib.hhg_ipc_open_handle(hr, ctypes.byref(pr)), "ipc_open_handle")
-            check(lib.hhg_ipc_open_handle(hf, ctypes.byref(pf)), "ipc_open_handle")
-            self.peer_recv[nb], self.peer_flag[nb] = pr.value, pf.value
-            self._opened += [pr.value, pf.value]
+        dist.all_gather_object(allh, (mine, err))
+        errs = [e for _, e in allh if e]
+        if not errs:
+            try:
+                for nb in self.nbrs:
+                    hr, hf = allh[nb][0][self.rank]     # nb's buffers that receive from me
+                    pr, pf = ctypes.c_void_p(), ctypes.c_void_p()
+                    check(lib.hhg_ipc_open_handle(hr, ctypes.byref(pr)), "ipc_open_handle")
+                    self._opened.append(pr.value)
+                    check(lib.hhg_ipc_open_handle(hf, ctypes.byref(pf)), "ipc_open_handle")
+                    self._opened.append(pf.value)
+                    self.peer_recv[nb], self.peer_flag[nb] = pr.value, pf.value
+            except Exception as exc:              # noqa: BLE001
+                err = f"rank {self.rank}: {exc}"
+            oks = [None] * dist.get_world_size()
+            dist.all_gather_object(oks, err)
+            errs = [e for e in oks if e]
+        if errs:
+            self.close()
+            raise PeerUnavailable("; ".join(errs))
 
     def connect_local(self, peers):
         """Single-process emulation: ``peers[nb]`` is the neighbour's
