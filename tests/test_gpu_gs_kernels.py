@@ -59,7 +59,7 @@ def check_skew_volume(variant: str, omega: float) -> None:
 def smooth_c3(out: str) -> None:
     from paper_1709_06793_b200 import Operator, RefinedGrid, sample_nodal
     from tests.cases import case_mesh, k_c3
-    grid = RefinedGrid(case_mesh("c3"), 5)
+    grid = RefinedGrid(case_mesh("c3"), 6)
     kf = sample_nodal(k_c3(), grid)
     rng = np.random.default_rng(3)
     u = rng.uniform(-1, 1, grid.n_nodes)
