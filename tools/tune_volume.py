@@ -56,7 +56,7 @@ for B, W, NS, MINB, EXPT, EXTRA in configs:
     dg = DeviceGrid(gt, kf.values)
     st = torch.cuda.current_stream().cuda_stream
     h.hhg_ghost_update(dg.ref, u.data_ptr(), st)
-    for fast in (0, 2, 4):
+    for fast in (int(x) for x in os.environ.get("FLAGS", "0 2 4 6").split()):
         for _ in range(3):
             h.hhg_volume_apply(dg.ref, 0, fast, sh.data_ptr(), None, u.data_ptr(), None, out.data_ptr(), st)
         torch.cuda.synchronize()
