@@ -271,6 +271,27 @@ def test_large_grid_algebraic_properties(cuda):
     s1 = torch.dot(y, Ax * free).item()
     s2 = torch.dot(x, Ay * free).item()
     assert abs(s1 - s2) <= 1e-10 * abs(s1)
+    # the smoother at full size (hyperplane-major whole-lattice sweep, one
+    # wave of clusters, grid surface sweep): two sweeps, then the volume
+    # rows of three elements re-swept by the C oracle from the GPU's own
+    # state after the second surface sweep are bitwise the GPU's
+    f = rng.uniform(-1, 1, grid.n_nodes)
+    df = torch.as_tensor(f, device="cuda")
+    du = torch.as_tensor(u, device="cuda")
+    op.smooth_device(du, df, sweeps=1)
+    mid = du.clone()
+    op.smooth_device(du, df, sweeps=1)
+    after = du.cpu().numpy()
+    surf = np.arange(grid.n_nodes) < grid.n_surface_nodes
+    u_mix = mid.cpu().numpy()
+    u_mix[surf] = after[surf]
+    vol_pos = grid.lat.index(M.SimplexLattice(3, grid.n - 4).coords + 1)
+    for t in (0, 47, 95):
+        uloc = np.ascontiguousarray(u_mix[grid.elem_gidx[t]])
+        s0 = int(grid.vol_start[t])
+        ok.gs_scaling_3d(grid.n, grid.lat.base, uloc, f[s0:s0 + nvol], kf.values[t], op._sh[t],
+                         1.0)
+        assert np.array_equal(after[s0:s0 + nvol], uloc[vol_pos]), t
 
 
 @pytest.mark.parametrize("name", ["scaling", "nodal", "hybrid:wv+we", "hybrid:wf"])
@@ -328,8 +349,9 @@ def test_surface_first_side_stream_path(cuda):
 def test_config5_full_size(cuda):
     """BASELINE config 5 at its full per-GPU size (96 macro elements, level 8,
     2.7e8 unknowns): constants are annihilated exactly on free rows, three
-    elements' volume rows are bitwise the C oracle's, and the operator is
-    linear and symmetric on the free nodes."""
+    elements' volume rows are bitwise the C oracle's, the operator is
+    linear and symmetric on the free nodes, and the smoother's volume rows
+    of three elements are bitwise the oracle's sweep from the same state."""
     from tests.cases import k_c5
     torch = cuda
     grid = M.RefinedGrid(case_mesh("c5"), 8)
@@ -357,6 +379,27 @@ def test_config5_full_size(cuda):
     s1 = torch.dot(y, Ax * free).item()
     s2 = torch.dot(x, Ay * free).item()
     assert abs(s1 - s2) <= 1e-10 * abs(s1)
+    # the smoother at full size (hyperplane-major whole-lattice sweep, one
+    # wave of clusters, grid surface sweep): two sweeps, then the volume
+    # rows of three elements re-swept by the C oracle from the GPU's own
+    # state after the second surface sweep are bitwise the GPU's
+    f = rng.uniform(-1, 1, grid.n_nodes)
+    df = torch.as_tensor(f, device="cuda")
+    du = torch.as_tensor(u, device="cuda")
+    op.smooth_device(du, df, sweeps=1)
+    mid = du.clone()
+    op.smooth_device(du, df, sweeps=1)
+    after = du.cpu().numpy()
+    surf = np.arange(grid.n_nodes) < grid.n_surface_nodes
+    u_mix = mid.cpu().numpy()
+    u_mix[surf] = after[surf]
+    vol_pos = grid.lat.index(M.SimplexLattice(3, grid.n - 4).coords + 1)
+    for t in (0, 47, 95):
+        uloc = np.ascontiguousarray(u_mix[grid.elem_gidx[t]])
+        s0 = int(grid.vol_start[t])
+        ok.gs_scaling_3d(grid.n, grid.lat.base, uloc, f[s0:s0 + nvol], kf.values[t], op._sh[t],
+                         1.0)
+        assert np.array_equal(after[s0:s0 + nvol], uloc[vol_pos]), t
 
 
 @pytest.mark.parametrize("name", ["scaling", "nodal", "const", "hybrid:wv+we", "stored"])
