@@ -858,17 +858,6 @@ __global__ void gs_surface_kernel(SurfGSDesc G) {
   if (e < G.count) gs_surface_row(G, G.level_rows[e]);   // recomputing form
 }
 
-// narrow sweeps: one CTA walks all levels, a block barrier between levels
-__global__ void __launch_bounds__(1024)
-gs_surface_block_kernel(SurfGSDesc G, const long long *level_ptr, int nlev) {
-  for (int lv = 0; lv < nlev; ++lv) {
-    const long long a = level_ptr[lv], b = level_ptr[lv + 1];
-    for (long long e = a + threadIdx.x; e < b; e += blockDim.x)
-      gs_surface_row_csr(G, G.level_rows[e]);
-    __syncthreads();
-  }
-}
-
 // Row of the surface sweep split in two: everything that does not depend
 // on u (row id, entry range, diagonal, f, the first PF column ids and
 // weights) is fetched before the grid barrier that precedes the row's
