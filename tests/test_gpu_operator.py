@@ -275,7 +275,10 @@ def test_large_grid_algebraic_properties(cuda):
     # wave of clusters, grid surface sweep): two sweeps, then the volume
     # rows of three elements re-swept by the C oracle from the GPU's own
     # state after the second surface sweep are bitwise the GPU's
+    rng = np.random.default_rng(5)
+    u = rng.uniform(-1, 1, grid.n_nodes)
     f = rng.uniform(-1, 1, grid.n_nodes)
+    nvol = grid.nodes_per_volume
     df = torch.as_tensor(f, device="cuda")
     du = torch.as_tensor(u, device="cuda")
     op.smooth_device(du, df, sweeps=1)
@@ -383,7 +386,10 @@ def test_config5_full_size(cuda):
     # wave of clusters, grid surface sweep): two sweeps, then the volume
     # rows of three elements re-swept by the C oracle from the GPU's own
     # state after the second surface sweep are bitwise the GPU's
+    rng = np.random.default_rng(5)
+    u = rng.uniform(-1, 1, grid.n_nodes)
     f = rng.uniform(-1, 1, grid.n_nodes)
+    nvol = grid.nodes_per_volume
     df = torch.as_tensor(f, device="cuda")
     du = torch.as_tensor(u, device="cuda")
     op.smooth_device(du, df, sweeps=1)
