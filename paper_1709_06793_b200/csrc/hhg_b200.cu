@@ -119,7 +119,8 @@ static int launch_mirror(const VolDesc &D, cudaStream_t st) {
   static_assert(kW == 4, "the mirror kernel uses 8x4-lane warps of 4B rows");
   constexpr int NW = HHG_MIRROR_NW;
   constexpr int ROWS = 4 * kB + 2;
-  const size_t smem = sizeof(double2) * kNS * ROWS * (8 * NW + 2);
+  const size_t smem = sizeof(double2) * kNS * ROWS *
+                      (HHG_VOL_SOA ? HHG_VOL_CS : 8 * NW + 2);
 #ifndef HHG_VOLUME_WS
 #define HHG_VOLUME_WS 0          // warp-specialised producer / consumer form
 #endif

@@ -20,9 +20,33 @@ namespace hhg {
 constexpr int VOL_COLS = 34;  // 32 lanes + halo
 
 // ablation switch for tools/tune_volume.py (0 in every product build):
-// 1 = no arithmetic (store v0), 2 = no staging after the prologue
+// 1 = no arithmetic (store v0), 2 = no staging after the prologue,
+// 3 = no stores, 4 = staging ring only (no window loads, arithmetic, stores)
 #ifndef HHG_VOL_EXPT
 #define HHG_VOL_EXPT 0
+#endif
+// experiments (tools/tune_volume.py): L2 prefetch distance of the tile rows
+// in planes (0 = off) and an L2 sector-promotion hint on the staging copies
+#ifndef HHG_VOL_PF
+#define HHG_VOL_PF 0
+#endif
+// ring layout of volume_kernel_mirror: 0 = interleaved (v, k) pairs (16-B
+// slots, one LDS.128 per window point; the 8-byte staging writes of a warp
+// are 16 B apart = 2x the shared wavefronts), 1 = separate v and k planes
+// with a padded row stride of HHG_VOL_CS doubles (contiguous staging writes;
+// two LDS.64 per window point)
+#ifndef HHG_VOL_SOA
+#define HHG_VOL_SOA 0
+#endif
+// FMA mode: split each row's accumulation into two chains
+#ifndef HHG_FMA_SPLIT
+#define HHG_FMA_SPLIT 0
+#endif
+#ifndef HHG_VOL_CS
+#define HHG_VOL_CS 40
+#endif
+#ifndef HHG_VOL_L2H
+#define HHG_VOL_L2H ""
 #endif
 
 struct VolDesc {
@@ -176,6 +200,20 @@ __device__ __forceinline__ void load_win(Win<B> &w, const double2 *slot, int r0,
   for (int m = 0; m < B + 1; ++m) w.R[m] = base[m * COLS + 1];
 #pragma unroll
   for (int m = 0; m < B + 1; ++m) w.L[m] = base[(m + 1) * COLS - 1];
+}
+
+// same window from separate v / k planes (row stride CS doubles)
+template <int B, int CS>
+__device__ __forceinline__ void load_win_soa(Win<B> &w, const double *v, const double *k,
+                                             int r0, int c) {
+  const int o = (r0 - 1) * CS + c;
+#pragma unroll
+  for (int m = 0; m < B + 2; ++m) w.C[m] = make_double2(v[o + m * CS], k[o + m * CS]);
+#pragma unroll
+  for (int m = 0; m < B + 1; ++m) w.R[m] = make_double2(v[o + m * CS + 1], k[o + m * CS + 1]);
+#pragma unroll
+  for (int m = 0; m < B + 1; ++m)
+    w.L[m] = make_double2(v[o + (m + 1) * CS - 1], k[o + (m + 1) * CS - 1]);
 }
 
 // gather the 14 neighbours of output row s from below / mid / above windows
@@ -723,6 +761,32 @@ __device__ __forceinline__ void fma_step(const Win<B> &mi, const Win<B> &hi,
 #pragma unroll
   for (int s = 0; s < B; ++s) {
     const double2 p = mi.C[s + 1];
+#if HHG_FMA_SPLIT
+    // two accumulation chains per row (in-plane / up-plane terms), summed
+    // at the end: half the dependent-latency chain per row
+    double acc = P[s];
+    double up = fflux(p, hi.C[s + 1], sh[2]);                // (0,0,1), shared with kk+1
+    Pn[s] = -up;
+    acc = fpair(p, mi.R[s + 1], mi.L[s], sh[0], acc);        // (1,0,0) (-1,0,0)
+    up = fterm(p, hi.R[s], sh[6], up);                       // (1,-1,1)
+    acc = fpair(p, mi.R[s], mi.L[s + 1], sh[3], acc);        // (1,-1,0) (-1,1,0)
+    up = fterm(p, hi.L[s], sh[4], up);                       // (-1,0,1)
+    if (s + 1 < B) {                                         // (0,1,0), shared with s+1
+      F1[s] = fflux(p, mi.C[s + 2], sh[1]);
+      acc += F1[s];
+    } else {
+      acc = fterm(p, mi.C[s + 2], sh[1], acc);
+    }
+    if (s >= 1) {                                            // (0,-1,1), shared with
+      const double F12 = fflux(p, hi.C[s], sh[5]);           // (0,1,-1) of row s-1 at kk+1
+      up += F12;
+      Pn[s - 1] -= F12;
+    } else {
+      up = fterm(p, hi.C[s], sh[5], up);
+    }
+    acc = (s >= 1) ? acc - F1[s - 1] : fterm(p, mi.C[s], sh[1], acc);   // (0,-1,0)
+    out[s] = acc + up;
+#else
     double acc = P[s];
     acc = fpair(p, mi.R[s + 1], mi.L[s], sh[0], acc);        // (1,0,0) (-1,0,0)
     acc = fpair(p, mi.R[s], mi.L[s + 1], sh[3], acc);        // (1,-1,0) (-1,1,0)
@@ -746,6 +810,7 @@ __device__ __forceinline__ void fma_step(const Win<B> &mi, const Win<B> &hi,
       acc = fterm(p, hi.C[s], sh[5], acc);
     }
     out[s] = acc;
+#endif
   }
 #pragma unroll
   for (int s = 0; s < B; ++s) {
@@ -767,7 +832,11 @@ volume_kernel_mirror(VolDesc D) {
   constexpr int COLS = 8 * NW + 2;
   constexpr int NT = 32 * NW;
   constexpr int NSLOT = (ROWS * COLS + NT - 1) / NT;
-  constexpr unsigned PLANE_BYTES = ROWS * COLS * sizeof(double2);
+  constexpr bool SOA = HHG_VOL_SOA != 0;
+  constexpr int CS = SOA ? HHG_VOL_CS : COLS;
+  static_assert(CS >= COLS, "padded stride below the tile width");
+  constexpr unsigned PLANE_BYTES = ROWS * CS * sizeof(double2);
+  constexpr unsigned KOFF = SOA ? ROWS * CS * sizeof(double) : sizeof(double);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2 *ring = reinterpret_cast<double2 *>(smem_raw);
   const unsigned ring_s = static_cast<unsigned>(__cvta_generic_to_shared(ring));
@@ -817,6 +886,7 @@ volume_kernel_mirror(VolDesc D) {
     int ko, vo, go;   // lattice, volume-block, ghost offsets at the next plane
     int pmax;         // last plane containing the point (i + j + p <= n)
     int ij;           // i | j << 16
+    unsigned so;      // byte offset of the slot's v inside a plane of the ring
   };
   IncSlot sl_[NSLOT];
 #pragma unroll
@@ -829,6 +899,7 @@ volume_kernel_mirror(VolDesc D) {
     sl_[m].ko = sj * (n + 1) - sj * (sj - 1) / 2 + si;                   // plane 0
     sl_[m].vo = (sj - 1) * (n - 3) - (sj - 1) * (sj - 2) / 2 + si - 1;    // plane 1
     sl_[m].go = sl_[m].ko;                                               // plane 0
+    sl_[m].so = SOA ? (unsigned)(r * CS + cc) * 8u : (unsigned)e * 16u;
   }
   const int t2n = (n + 1) * (n + 2) / 2;
   auto produce = [&](int p) {
@@ -846,12 +917,12 @@ volume_kernel_mirror(VolDesc D) {
         const bool interior = p >= 1 && si >= 1 && sj >= 1 && p < S.pmax;
         const double *vs = interior ? at(T.v, S.vo) : at(T.g, S.go);
         const double *ks = at(T.k, S.ko);
-        const unsigned d = off + (unsigned)(threadIdx.x + m * NT) * sizeof(double2);
+        const unsigned d = off + S.so;
         asm volatile(
             "{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n"
-            " @q cp.async.ca.shared.global [%0], [%1], 8;\n"
-            " @q cp.async.ca.shared.global [%2], [%3], 8;\n}\n" ::"r"(d),
-            "l"(vs), "r"(d + 8), "l"(ks), "r"(live));
+            " @q cp.async.ca.shared.global" HHG_VOL_L2H " [%0], [%1], 8;\n"
+            " @q cp.async.ca.shared.global" HHG_VOL_L2H " [%2], [%3], 8;\n}\n" ::"r"(d),
+            "l"(vs), "r"(d + KOFF), "l"(ks), "r"(live));
       }
       // advance to plane p + 1
       S.ko += (n - p + 1) * (n - p) / 2 + (n - p + 1) - sj;   // T2(n - p) - j
@@ -862,6 +933,27 @@ volume_kernel_mirror(VolDesc D) {
         S.go += 3 * (n - p) - (sj > 0 ? 1 : 0);
     }
     mbar_arrive_cp_async(full0 + 8 * sl);
+#if HHG_VOL_PF > 0
+    // experiment: L2 prefetch of the tile's rows HHG_VOL_PF planes ahead
+    // (4 lines per 34-point row segment, k and v rows: 112 threads)
+    {
+      const int q = p + HHG_VOL_PF;
+      if (SRC == SRC_SPLIT && q <= kmax + 1 && threadIdx.x < 112) {
+        const int seg = threadIdx.x >> 2, part = threadIdx.x & 3;
+        const int sj = j0 - 1 + (seg >> 1);
+        int si = i0 - 1 + part * 11;
+        if (seg & 1) {
+          si = min(si, n - 1 - sj - q);
+          if (q >= 1 && sj >= 1 && si >= 1 && si >= i0 - 1)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(at(T.v, lbase32(n - 4, q - 1, sj - 1) + si - 1)));
+        } else {
+          si = min(si, n - sj - q);
+          if (si >= i0 - 1 && sj >= 0)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(at(T.k, lbase32(n, q, sj) + si)));
+        }
+      }
+    }
+#endif
   };
 
   for (int p = 0; p < PD && p <= kmax + 1; ++p) produce(p);
@@ -888,7 +980,12 @@ volume_kernel_mirror(VolDesc D) {
   auto fetch = [&](int q, Win<B> &w) {
     const int sl = q % NS;
     mbar_wait(full0 + 8 * sl, (q / NS) & 1);
-    load_win<B, COLS>(w, ring + sl * ROWS * COLS, r0, c);
+    if constexpr (SOA) {
+      const double *pv = reinterpret_cast<const double *>(smem_raw + sl * PLANE_BYTES);
+      load_win_soa<B, CS>(w, pv, pv + ROWS * CS, r0, c);
+    } else {
+      load_win<B, COLS>(w, ring + sl * ROWS * COLS, r0, c);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty0 + 8 * sl);
     if (q + PD <= kmax + 1) produce(q + PD);
@@ -913,6 +1010,7 @@ volume_kernel_mirror(VolDesc D) {
   // output plane kk = q - 1 from mi (plane kk) and hi (plane kk + 1)
   auto step = [&](int q, Win<B> &mi, Win<B> &hi) {
     fetch(q, hi);
+    if constexpr (HHG_VOL_EXPT == 4) return;       // ablation: staging ring only
     if (warp_min_ij <= n - q) {   // some lane of the warp is valid
       double vals[B];
       if constexpr (HHG_VOL_EXPT == 1) {          // data movement only

@@ -38,7 +38,8 @@ sh = torch.as_tensor(np.stack([reference_stencil(grid, t)[1] / 2 for t in range(
 nvol = grid.nodes_per_volume * grid.macro.n_elements
 ref = None
 for B, W, NS, MINB, EXPT, EXTRA in configs:
-    so = f"/tmp/hhg_tune_{B}_{W}_{NS}_{MINB}_{EXPT}_{'_'.join(EXTRA)}.so"
+    tag = "".join(ch if ch.isalnum() else "_" for ch in "_".join(EXTRA))
+    so = f"/tmp/hhg_tune_{B}_{W}_{NS}_{MINB}_{EXPT}_{tag}.so"
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
            "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC", "-shared", "-DHHG_SCALING_ONLY",
            f"-DHHG_VOL_B={B}", f"-DHHG_VOL_W={W}", f"-DHHG_VOL_NS={NS}", f"-DHHG_VOL_MINB={MINB}", f"-DHHG_MIRROR_MINB={MINB}", f"-DHHG_VOL_EXPT={EXPT}", *[f"-D{e}" for e in EXTRA], "-Xptxas", "-v",
