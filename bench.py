@@ -142,13 +142,21 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+SETUP = {}
+
+
 def build_workload(rank, world, level, nx, variant, fast):
     from paper_1709_06793_b200 import Operator, RefinedGrid, sample_nodal
     from paper_1709_06793_b200.shard import InterfaceMap, slab_mesh
     from tests.cases import k_c5
+    t0 = time.time()
     grid = RefinedGrid(slab_mesh(rank, world, nx, nx), level)
-    kf = sample_nodal(k_c5(), grid)
+    t1 = time.time()
+    kf = sample_nodal(k_c5(), grid)     # the synthetic coefficient (numpy, host)
+    t2 = time.time()
     op = Operator(grid, variant, kf, fast=fast)
+    SETUP.update(grid_s=round(t1 - t0, 2), coefficient_s=round(t2 - t1, 2),
+                 operator_s=round(time.time() - t2, 2))
     u = np.random.default_rng(1234 + rank).uniform(-1.0, 1.0, grid.n_nodes)
     imap = InterfaceMap(grid, rank, world, 1.0 / nx) if world > 1 else None
     if imap is not None:   # interface copies must agree across ranks
@@ -182,7 +190,10 @@ def run_own(args):
     # GPU work the host measured up to 1.5x slower in round 1)
     cpu = None
     if rank == 0 and world == 1:
+        t_cpu = time.time()
         cpu = cpu_baseline(grid, kf, op, u, args.cpu_tets, reps=3)
+        t_setup += time.time() - t_cpu        # not part of the set-up
+    t_dev = time.time()
     D = op._device()
     du = torch.as_tensor(u, device="cuda")
     out = torch.empty_like(du)
@@ -199,6 +210,7 @@ def run_own(args):
             args.exchange = "nccl"
             sop = ShardedOperator(op, imap, dist, grid.dirichlet_mask, transport="nccl")
     torch.cuda.synchronize()
+    SETUP["device_s"] = round(time.time() - t_dev, 2)
     t_setup = time.time() - t_setup
 
     vol_ev = []
@@ -332,7 +344,7 @@ def run_own(args):
             "all_rows_gdofs": round(grid.n_nodes * world / (ms * 1e-3) / 1e9, 3),
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
-            "setup_s": round(t_setup, 1),
+            "setup_s": round(t_setup, 1), "setup": dict(SETUP),
             "build": lib.hhg_build_info().decode(),
         }
         print(json.dumps(line), flush=True)
