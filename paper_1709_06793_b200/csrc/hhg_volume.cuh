@@ -21,7 +21,8 @@ constexpr int VOL_COLS = 34;  // 32 lanes + halo
 
 // ablation switch for tools/tune_volume.py (0 in every product build):
 // 1 = no arithmetic (store v0), 2 = no staging after the prologue,
-// 3 = no stores, 4 = staging ring only (no window loads, arithmetic, stores)
+// 3 = no stores, 4 = staging ring only (no window loads, arithmetic, stores),
+// 5 = k not staged (v only; timing of a k path off the LSU)
 #ifndef HHG_VOL_EXPT
 #define HHG_VOL_EXPT 0
 #endif
@@ -918,14 +919,21 @@ volume_kernel_mirror(VolDesc D) {
         const double *vs = interior ? at(T.v, S.vo) : at(T.g, S.go);
         const double *ks = at(T.k, S.ko);
         const unsigned d = off + S.so;
-        asm volatile(
-            "{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n"
-            " @q cp.async.ca.shared.global" HHG_VOL_L2H " [%0], [%1], 8;\n"
-            " @q cp.async.ca.shared.global" HHG_VOL_L2H " [%2], [%3], 8;\n}\n" ::"r"(d),
-            "l"(vs), "r"(d + KOFF), "l"(ks), "r"(live));
+        if constexpr (HHG_VOL_EXPT == 5) {   // ablation: v staged, k not (timing only)
+          asm volatile(
+              "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
+              " @q cp.async.ca.shared.global [%0], [%1], 8;\n}\n" ::"r"(d),
+              "l"(vs), "r"(live));
+        } else {
+          asm volatile(
+              "{\n .reg .pred q;\n setp.ne.b32 q, %4, 0;\n"
+              " @q cp.async.ca.shared.global" HHG_VOL_L2H " [%0], [%1], 8;\n"
+              " @q cp.async.ca.shared.global" HHG_VOL_L2H " [%2], [%3], 8;\n}\n" ::"r"(d),
+              "l"(vs), "r"(d + KOFF), "l"(ks), "r"(live));
+        }
       }
       // advance to plane p + 1
-      S.ko += (n - p + 1) * (n - p) / 2 + (n - p + 1) - sj;   // T2(n - p) - j
+      if (HHG_VOL_EXPT != 5) S.ko += (n - p + 1) * (n - p) / 2 + (n - p + 1) - sj;   // T2(n - p) - j
       if (p >= 1) S.vo += (n - 2 - p) * (n - 1 - p) / 2 - (sj - 1);  // T2(n-3-p) - (j-1)
       if (p == 0)
         S.go = t2n + (sj == 0 ? si : n + 2 * (sj - 1) + (si > 0 ? 1 : 0));
