@@ -312,6 +312,15 @@ int hhg_restrict(const hhg_transfer *T, const double *xf, double *yc, void *stre
 /* y[ids[e]] = 0 (coarse Dirichlet rows after restriction) */
 int hhg_scatter_zero(int64_t n, const int64_t *ids, double *y, void *stream);
 
+/* interface exchange over NCCL (shard.exchange_partials; the reference has
+ * no distributed path - its single-domain apply is operators.py:485-499):
+ * y[e] = x[ids[e]] packs a rank's one-sided interface rows (mine) for the
+ * send; out[ids[e]] = recv[e] + mine[e] (recv_first) or mine[e] + recv[e]
+ * completes them in rank order, so both ranks hold bitwise equal rows */
+int hhg_gather(int64_t n, const int64_t *ids, const double *x, double *y, void *stream);
+int hhg_interface_add(int64_t n, const int64_t *ids, const double *mine, const double *recv,
+                      int recv_first, double *out, void *stream);
+
 /* smoother pieces (Operator.smooth): one level of the level-scheduled
  * surface Gauss-Seidel (rows given as indices into s->rows), and the volume
  * hyperplane wavefronts of all macro elements (reads the ghost layer, which

@@ -183,6 +183,8 @@ EXPORTS = {
     "hhg_prolongate": (ctypes.c_int, [ctypes.POINTER(HhgTransfer), vp, vp, ctypes.c_int, vp]),
     "hhg_restrict": (ctypes.c_int, [ctypes.POINTER(HhgTransfer), vp, vp, vp]),
     "hhg_scatter_zero": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp]),
+    "hhg_gather": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, vp]),
+    "hhg_interface_add": (ctypes.c_int, [ctypes.c_int64, vp, vp, vp, ctypes.c_int, vp, vp]),
     "hhg_status": (ctypes.c_int, []),
     "hhg_status_reset": (ctypes.c_int, []),
     "hhg_build_info": (ctypes.c_char_p, []),

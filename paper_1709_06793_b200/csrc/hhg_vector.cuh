@@ -186,6 +186,18 @@ __global__ void scatter_zero_kernel(long long n, const long long *ids, double *y
   if (e < n) y[ids[e]] = 0.0;
 }
 
+// interface exchange over NCCL (shard.exchange_partials): pack the
+// one-sided interface rows, then complete them in rank order
+__global__ void gather_kernel(long long n, const long long *ids, const double *x, double *y) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < n) y[e] = x[ids[e]];
+}
+__global__ void interface_add_kernel(long long n, const long long *ids, const double *mine,
+                                     const double *recv, int recv_first, double *out) {
+  const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (e < n) out[ids[e]] = recv_first ? dadd(recv[e], mine[e]) : dadd(mine[e], recv[e]);
+}
+
 }  // namespace hhg
 
 extern "C" {
@@ -325,6 +337,24 @@ int hhg_restrict(const hhg_transfer *T, const double *xf, double *yc, void *stre
     return check("scatter_zero_kernel");
   }
   return HHG_OK;
+}
+
+int hhg_gather(int64_t n, const int64_t *ids, const double *x, double *y, void *stream) {
+  if (n <= 0) return HHG_OK;
+  if (!ids || !x || !y) return HHG_ERR_ARG;
+  hhg::gather_kernel<<<(int)((n + 255) / 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      n, reinterpret_cast<const long long *>(ids), x, y);
+  return check("gather_kernel");
+}
+
+int hhg_interface_add(int64_t n, const int64_t *ids, const double *mine, const double *recv,
+                      int recv_first, double *out, void *stream) {
+  if (n <= 0) return HHG_OK;
+  if (!ids || !mine || !recv || !out) return HHG_ERR_ARG;
+  hhg::interface_add_kernel<<<(int)((n + 255) / 256), 256, 0,
+                              reinterpret_cast<cudaStream_t>(stream)>>>(
+      n, reinterpret_cast<const long long *>(ids), mine, recv, recv_first, out);
+  return check("interface_add_kernel");
 }
 
 int hhg_scatter_zero(int64_t n, const int64_t *ids, double *y, void *stream) {

@@ -91,12 +91,23 @@ def exchange_partials(out, imap: InterfaceMap, dist, index_tensors=None):
         return out
     # gloo moves host tensors only: stage device vectors through host memory
     stage = out.is_cuda and dist.get_backend() == "gloo"
+    native = out.is_cuda and not stage and out.dtype == torch.float64
+    if native:
+        from ._lib import check, lib
+        st = torch.cuda.current_stream().cuda_stream
     ops, recv, ids_t = [], {}, {}
     for nbr, ids in imap.neighbours.items():
         idx = index_tensors[nbr] if index_tensors is not None else \
             torch.as_tensor(ids, device=out.device)
+        if native:
+            idx = idx.to(torch.int64).contiguous()
         ids_t[nbr] = idx
-        send = out.index_select(0, idx).contiguous()
+        if native:      # pack with the library's gather kernel
+            send = torch.empty(len(idx), dtype=out.dtype, device=out.device)
+            check(lib.hhg_gather(len(idx), idx.data_ptr(), out.data_ptr(), send.data_ptr(), st),
+                  "gather")
+        else:
+            send = out.index_select(0, idx).contiguous()
         if stage:
             send = send.cpu()
         buf = torch.empty_like(send)
@@ -106,6 +117,11 @@ def exchange_partials(out, imap: InterfaceMap, dist, index_tensors=None):
     for req in dist.batch_isend_irecv(ops):
         req.wait()
     for nbr, (mine, theirs) in recv.items():
+        if native:      # out[ids] = theirs + mine (lower rank first), in place
+            check(lib.hhg_interface_add(len(ids_t[nbr]), ids_t[nbr].data_ptr(), mine.data_ptr(),
+                                        theirs.data_ptr(), int(nbr < imap.rank), out.data_ptr(),
+                                        st), "interface_add")
+            continue
         total = (theirs + mine) if nbr < imap.rank else (mine + theirs)
         out.index_copy_(0, ids_t[nbr], total.to(out.device))
     return out

@@ -122,3 +122,26 @@ def test_peer_exchange_ipc_two_processes(cuda):
         assert np.abs(out - ref[gids]).max() <= 1e-13 * np.abs(ref).max()
     (_, X0, o0, n0), (_, X1, o1, n1) = res
     assert np.array_equal(o0[n0[1]], o1[n1[0]])
+
+
+def test_nccl_pack_and_rank_order_add_kernels(cuda):
+    """The NCCL transport's native pieces (hhg_gather, hhg_interface_add)
+    reproduce index_select and the rank-ordered sums of the torch path
+    bitwise (NCCL itself needs two GPUs; the kernels do not)."""
+    torch = cuda
+    from paper_1709_06793_b200._lib import check, lib
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    out = torch.rand(10_000, dtype=torch.float64, device="cuda", generator=gen)
+    ids = torch.randperm(10_000, device="cuda", generator=gen)[:3_001].to(torch.int64)
+    theirs = torch.rand(3_001, dtype=torch.float64, device="cuda", generator=gen) * 1e3
+    st = torch.cuda.current_stream().cuda_stream
+    mine = torch.empty(3_001, dtype=torch.float64, device="cuda")
+    check(lib.hhg_gather(3_001, ids.data_ptr(), out.data_ptr(), mine.data_ptr(), st), "gather")
+    assert torch.equal(mine, out.index_select(0, ids))
+    for first in (0, 1):
+        got = out.clone()
+        check(lib.hhg_interface_add(3_001, ids.data_ptr(), mine.data_ptr(), theirs.data_ptr(),
+                                    first, got.data_ptr(), st), "interface_add")
+        want = out.clone()
+        want.index_copy_(0, ids, (theirs + mine) if first else (mine + theirs))
+        assert torch.equal(got, want)
