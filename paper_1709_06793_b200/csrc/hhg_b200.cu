@@ -1027,7 +1027,8 @@ int hhg_smooth_surface_all(const hhg_grid *g, const hhg_surface *s, const hhg_su
   if (slots) {
     static std::map<int, int> gcaps;
     const int cap = device_capacity(gs_surface_slots_kernel<true>, HHG_SURF_GRID_CT, gcaps);
-    int blocks = (int)std::min<long long>((mean_width + 7) / 8, cap);
+    int blocks = (int)std::min<long long>((mean_width + HHG_SURF_GRID_RPB - 1) / HHG_SURF_GRID_RPB,
+                                          cap);
     if (blocks < 8) blocks = std::min(8, cap);
     unsigned *bar = gs->sweep_bar;
     cudaError_t e = cudaMemsetAsync(bar, 0, sizeof(unsigned), S(stream));

@@ -1039,6 +1039,12 @@ __global__ void surface_slots_kernel(SurfGSDesc G, long long *gid, int *cnt, dou
   dyn[e] = (int)bits;
 }
 
+#ifndef HHG_SURF_BAR
+#define HHG_SURF_BAR 1           // grid barrier arrive: 0 fence + atomicAdd, 1 red.release
+#endif
+#ifndef HHG_SURF_GRID_RPB
+#define HHG_SURF_GRID_RPB 8      // grid surface sweep: mean level rows per CTA
+#endif
 #ifndef HHG_SURF_CT
 #define HHG_SURF_CT 256          // threads per CTA of the cluster surface sweep
 #endif
@@ -1073,8 +1079,13 @@ gs_surface_slots_kernel(SurfGSDesc G, const long long *level_ptr, int nlev, unsi
     if constexpr (GRID) {
       __syncthreads();
       if (threadIdx.x == 0) {
+#if HHG_SURF_BAR == 1
+        // release reduction (fence.acq_rel + red) instead of a full fence
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+#else
         __threadfence();
         atomicAdd(bar, 1u);
+#endif
       }
     } else {
       asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
