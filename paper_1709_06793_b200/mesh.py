@@ -40,7 +40,7 @@ __all__ = [
     "SimplexLattice", "refine_uniform", "lattice_elements", "load_macro_mesh",
     "reference_simplex", "unit_cube_6", "unit_cube_12", "cylinder_shell_box",
     "kuhn_blocks", "DIRS_3D", "LOCAL_EDGES_3D", "LOCAL_FACES_3D",
-    "lattice_base", "lattice_size",
+    "lattice_base", "lattice_size", "classify_primitives", "neighborhood",
 ]
 
 # The 14 stencil directions of an interior lattice node, (di, dj, dk); the
@@ -580,3 +580,19 @@ class RefinedGrid:
 
 def refine_uniform(mesh: MacroMesh, level: int) -> RefinedGrid:
     return RefinedGrid(mesh, level)
+
+
+def classify_primitives(grid: "RefinedGrid"):
+    """Number of nodes owned by each primitive kind, keyed by the lower-case
+    kind name (mesh.py:748-752 of the reference)."""
+    counts = np.bincount(grid.node_kind.astype(np.int64), minlength=len(PrimitiveKind))
+    return {PrimitiveKind(k).name.lower(): int(c) for k, c in enumerate(counts) if c}
+
+
+def neighborhood(grid: "RefinedGrid", t: int) -> np.ndarray:
+    """Physical offsets of the 14 stencil neighbours of an interior node of
+    macro element t: the lattice directions through the element's edge
+    vectors, divided by the refinement n (mesh.py:755-765)."""
+    V = np.asarray(grid.macro.vertices, dtype=np.float64)[np.asarray(grid.macro.elements[t])]
+    return (DIRS_3D @ (V[1:] - V[0])) / grid.n
+

@@ -126,3 +126,25 @@ def test_coefficient_sampling_and_kmin_bitwise(tag, make, lvl, kname):
     kf = sample_nodal(kfn, grid)
     assert np.array_equal(kf.values, g[f"{tag}_values"])
     assert np.array_equal(kmin_field(kf).values, g[f"{tag}_kmin"])
+
+
+def test_classify_primitives_and_neighborhood():
+    """mesh.classify_primitives / neighborhood (reference mesh.py:748-765):
+    node counts per owner kind follow the refinement formulas; the stencil
+    offsets of an interior node are the lattice directions through the
+    element's edge vectors, mirror pairs opposite."""
+    from paper_1709_06793_b200 import mesh as Mm
+    grid = Mm.RefinedGrid(Mm.unit_cube_6(), 3)
+    n, mm = grid.n, grid.macro
+    counts = Mm.classify_primitives(grid)
+    ne = len(np.unique(np.sort(np.asarray(mm.elements)[:, [[0, 1], [0, 2], [0, 3], [1, 2], [1, 3], [2, 3]]], axis=2).reshape(-1, 2), axis=0))
+    assert counts["vertex"] == len(mm.vertices)
+    assert counts["edge"] == ne * (n - 1)
+    assert counts["volume"] == mm.n_elements * (n - 1) * (n - 2) * (n - 3) // 6
+    assert sum(counts.values()) == grid.n_nodes
+    for t in range(mm.n_elements):
+        off = Mm.neighborhood(grid, t)
+        assert off.shape == (14, 3)
+        assert np.array_equal(off[:7], -off[7:])
+        V = np.asarray(mm.vertices, dtype=float)[np.asarray(mm.elements[t])]
+        assert np.allclose(off[0], (V[1] - V[0]) / n)
