@@ -319,15 +319,9 @@ def run_own(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded u, analytic k)",
-            "config": {"workload": f"config 5 per GPU: 4x4x1 Kuhn-cube slab, 96 macro tets, "
-                                   f"level {args.level}", "level": args.level,
-                       "macro_tets_per_gpu": ntets, "dofs_per_gpu": int(grid.n_nodes),
-                       "volume_dofs_per_gpu": int(nvol_rank), "variant": args.variant,
-                       "arithmetic": arith,
-                       "parallelism": f"macro-tet slabs x{world}"
-                                      + (f", {args.exchange} interface exchange" if world > 1
-                                         else ""),
-                       "l2": "inputs larger than L2 (2.2 GB per vector)"},
+            "config": workload_config(args, grid, world),
+            "arithmetic": arith,
+            "exchange": args.exchange if world > 1 else None,
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                          "unit": "GB/s", "frac": round(achieved / hbm, 4),
                          "traffic": traffic, "peak_kind": hbm_kind,
@@ -432,6 +426,18 @@ def cpu_baseline(grid, kf, op, u, ntets_sample, reps=2):
                       f"per step, best of {reps}, volume rows, all host threads"}
 
 
+def workload_config(args, grid, world):
+    """The workload both arms (own / --impl reference) report: identical
+    dicts for the same flags (the arithmetic mode is a separate key)."""
+    ntets = grid.macro.n_elements
+    return {"workload": f"config 5 per GPU: 4x4x1 Kuhn-cube slab, {ntets} macro tets, "
+                        f"level {args.level}", "level": args.level,
+            "macro_tets_per_gpu": ntets, "dofs_per_gpu": int(grid.n_nodes),
+            "volume_dofs_per_gpu": int(grid.nodes_per_volume * ntets), "variant": args.variant,
+            "parallelism": f"macro-tet slabs x{world}",
+            "l2": "inputs larger than L2 (2.2 GB per vector)"}
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU algorithm for this path (the C
     restatement of its numba kernel — the reference itself is Python/numba
@@ -466,8 +472,8 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded u, analytic k)",
-            "config": {"workload": f"config 5 per GPU: 4x4x1 Kuhn-cube slab, 96 macro tets, "
-                                   f"level {args.level}", "level": args.level},
+            "config": workload_config(args, grid, world),
+            "arithmetic": "bitwise reference order (C restatement of kernels.apply_scaling_3d)",
             "cpu_baseline": {"value": round(val, 4), "unit": "GDoF/s", "cores": threads,
                              "kind": "port", "cpu_model": cpu_model(),
                              "host_cpus": os.cpu_count(),
