@@ -15,7 +15,10 @@ __all__ = ["lib", "LIB_PATH", "HhgGrid", "HhgSurface", "HhgSurfaceGS", "HhgFace"
            "HhgError",
            "VAR", "FLAG_RESIDUAL", "FLAG_FAST", "FLAG_MIRROR", "EXPORTS"]
 
-LIB_PATH = Path(__file__).resolve().parent / "libhhg_b200.so"
+# HHG_LIB selects another build of the library (e.g. the bounds-checked
+# debug build of tools/bounds_check.sh); default: the in-tree product build
+LIB_PATH = Path(os.environ.get("HHG_LIB") or
+                Path(__file__).resolve().parent / "libhhg_b200.so").resolve()
 
 HHG_OK, HHG_ERR_ARG, HHG_ERR_CUDA, HHG_ERR_ZERO_DIAG, HHG_ERR_TABLE = 0, -1, -2, -3, -4
 VAR = {"scaling": 0, "nodal": 1, "const": 2, "stored": 3}

@@ -3,6 +3,28 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+// Bounds-checked debug build (-DHHG_DEBUG_BOUNDS=1; tools/bounds_check.sh):
+// compute-sanitizer is closed on this GPU pool, so the hot kernels assert
+// every global index they form against the extent of its array and trap
+// with the offending value.  Compiled out (no code) in product builds.
+#ifndef HHG_DEBUG_BOUNDS
+#define HHG_DEBUG_BOUNDS 0
+#endif
+#if HHG_DEBUG_BOUNDS
+#include <cstdio>
+#define HHG_BOUND(idx, lo, hi, what)                                                   \
+  do {                                                                                 \
+    const long long _i = (long long)(idx), _lo = (long long)(lo), _hi = (long long)(hi); \
+    if (_i < _lo || _i >= _hi) {                                                       \
+      printf("hhg bounds: %s = %lld outside [%lld, %lld) (block %d, thread %d)\n", what, \
+             _i, _lo, _hi, (int)blockIdx.x, (int)threadIdx.x);                         \
+      __trap();                                                                        \
+    }                                                                                  \
+  } while (0)
+#else
+#define HHG_BOUND(idx, lo, hi, what) ((void)0)
+#endif
+
 namespace hhg {
 
 // ---------------------------------------------------------------------------

@@ -448,9 +448,12 @@ gs_volume_skew_kernel(GSDesc D, double *us, const double *__restrict__ fs,
       const int di = c_dirs_h(d, 0), dj = c_dirs_h(d, 1), dk = c_dirs_h(d, 2);
       const int hq = h + di + 2 * dj + 3 * dk;
       const int pos = st_ring[(hq & 7) * srl + k + dk] + j + dj;
+      HHG_BOUND(pos, 0, D.L, "skewed sweep: neighbour position");
       q[d] = make_double2(__ldcg(ue + pos), __ldg(ke + pos));
     }
     const int self = st_ring[(h & 7) * srl + k] + j;
+    HHG_BOUND(self, 0, D.L, "skewed sweep: point position");
+    HHG_BOUND(e, 0, D.nvol, "skewed sweep: list index");
     const double old = __ldcg(ue + self), k0 = __ldg(ke + self), fv = __ldg(fe + e);
     double acc = 0.0, diag = 0.0;
     if (VAR == 0) {

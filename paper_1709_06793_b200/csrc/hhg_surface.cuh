@@ -170,7 +170,10 @@ __global__ void ghost_kernel(long long total, const long long *gid,
                              const double *u, double *ghost) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x)
+  {
+    HHG_BOUND(gid[e], 0, 1LL << 40, "ghost update: global id");
     ghost[e] = __ldg(u + gid[e]);
+  }
 }
 
 }  // namespace hhg

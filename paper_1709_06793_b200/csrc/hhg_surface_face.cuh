@@ -44,6 +44,7 @@ surface_face_kernel(SurfGSDesc G, const hhg_surface s, double *out, SurfPush pus
   constexpr int NONE = -(1 << 20);   // direction leaving the element
   const SurfDesc &D = G.s;
   const int4 tl = reinterpret_cast<const int4 *>(s.face_tiles)[blockIdx.x];
+  HHG_BOUND(tl.x, 0, s.nfaces, "face tile: face index");
   if (threadIdx.x < sizeof(hhg_face) / 4)
     reinterpret_cast<int *>(&F)[threadIdx.x] =
         reinterpret_cast<const int *>(s.faces + tl.x)[threadIdx.x];
@@ -66,7 +67,9 @@ surface_face_kernel(SurfGSDesc G, const hhg_surface s, double *out, SurfPush pus
       continue;
     }
     const long long idx = layer0 + (long long)l * sq * sq + (long long)(b0 + rb) * sq + (a0 + ra);
+    HHG_BOUND(idx - layer0, 0, 3LL * sq * sq, "face staging: layer index");
     const double kv = __ldg(s.face_k + idx);
+    HHG_BOUND(__ldg(s.face_g + idx), 0, 0xffffffffLL, "face staging: global id");
     const double v = __ldg(D.u + (unsigned)__ldg(s.face_g + idx));
     Ls[x] = make_double2(v, kv);
   }
@@ -85,6 +88,7 @@ surface_face_kernel(SurfGSDesc G, const hhg_surface s, double *out, SurfPush pus
 #pragma unroll
     for (int d = 0; d < 14; ++d) {
       const int o = offs[e][d];
+      if (o != NONE) HHG_BOUND(ctr + o, 0, 3 * AREA, "face row: staged neighbour");
       q[d] = o == NONE ? make_double2(v0, 0.0) : Ls[ctr + o];
     }
     double part;
@@ -105,6 +109,7 @@ surface_face_kernel(SurfGSDesc G, const hhg_surface s, double *out, SurfPush pus
   // (a, b) = the barycentrics of the face's 2nd and 3rd sorted vertices)
   const long long off = (long long)(b - 1) * (n - 2) - (long long)(b - 1) * (b - 2) / 2 + a - 1;
   const long long gid = F.fs + off;
+  HHG_BOUND(off, 0, (long long)(n - 2) * (n - 1) / 2, "face row: face-local offset");
   if (RES) row = dsub(D.f[gid], row);
   out[gid] = row;
   if (!RES && push.slot) {

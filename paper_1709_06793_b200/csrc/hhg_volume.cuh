@@ -919,6 +919,12 @@ volume_kernel_mirror(VolDesc D) {
         const double *vs = interior ? at(T.v, S.vo) : at(T.g, S.go);
         const double *ks = at(T.k, S.ko);
         const unsigned d = off + S.so;
+        if (live) {
+          HHG_BOUND(S.ko, 0, D.L, "volume staging: lattice offset");
+          if (interior) HHG_BOUND(S.vo, 0, D.nvol, "volume staging: volume-block offset");
+          else if (SRC == SRC_SPLIT) HHG_BOUND(S.go, 0, D.S, "volume staging: ghost offset");
+          HHG_BOUND(d + KOFF + 8 - ring_s, 0, NS * PLANE_BYTES + 1, "volume staging: ring byte");
+        }
         if constexpr (HHG_VOL_EXPT == 5) {   // ablation: v staged, k not (timing only)
           asm volatile(
               "{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n"
@@ -1006,6 +1012,7 @@ volume_kernel_mirror(VolDesc D) {
     for (int s = 0; s < B; ++s)
       if (i + jw + s <= lim) {
         const int cidx = iplane + (jw + s - 1) * rowi + oterm[s];
+        HHG_BOUND(cidx, 0, D.nvol, "volume emit: output row");
         double val = vals[s];
         if (RES) val = dsub(__ldg(at(T.f, cidx)), val);
         if (HHG_VOL_EXPT == 3) {                 // ablation: no stores
