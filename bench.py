@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--variant", default="scaling", choices=["scaling", "nodal"])
     ap.add_argument("--fast", action="store_true",
                     help="FMA / mirror-pair arithmetic (default: bitwise reference order)")
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N > 1 interface exchange: peer-memory push fused into the "
                          "surface-row kernel (CUDA IPC over NVLink) or NCCL send/recv")
