@@ -40,6 +40,9 @@ constexpr int VOL_COLS = 34;  // 32 lanes + halo
 #define HHG_VOL_SOA 0
 #endif
 // FMA mode: split each row's accumulation into two chains
+#ifndef HHG_SH_SMEM
+#define HHG_SH_SMEM 0
+#endif
 #ifndef HHG_FMA_SPLIT
 #define HHG_FMA_SPLIT 0
 #endif
@@ -861,9 +864,17 @@ volume_kernel_mirror(VolDesc D) {
     T.o = opaque(D.out + (long long)t * D.nvol);
     T.f = RES ? opaque(D.f + (long long)t * D.nvol) : nullptr;
   }
+#if HHG_SH_SMEM
+  // the element's 7 stencil constants in shared memory: under register
+  // pressure the compiler re-reads them (broadcast LDS) instead of spilling
+  __shared__ double s_sh[7];
+  if (threadIdx.x < 7) s_sh[threadIdx.x] = __ldg(D.coef + (long long)t * D.coef_stride + threadIdx.x);
+  const double (&sh)[7] = s_sh;
+#else
   double sh[7];
 #pragma unroll
   for (int d = 0; d < 7; ++d) sh[d] = __ldg(D.coef + (long long)t * D.coef_stride + d);
+#endif
 
   constexpr int PD = NS - 2;
   __shared__ __align__(8) unsigned long long bars[2 * NS];
