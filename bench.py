@@ -311,8 +311,12 @@ def run_own(args):
 
     if rank == 0:
         flags = op._vol_flags()
-        arith = ("fma edge-flux, mirror edge reuse (<= 1e-12 of the reference order)"
-                 if flags & 2 else "bitwise-reference-order, mirror edge reuse")
+        if args.variant == "nodal":
+            arith = ("fma term sums (<= 1e-12 of the reference order)" if flags & 2
+                     else "bitwise-reference-order")
+        else:
+            arith = ("fma edge-flux, mirror edge reuse (<= 1e-12 of the reference order)"
+                     if flags & 2 else "bitwise-reference-order, mirror edge reuse")
         line = {
             "metric": "GDoF/s of scaled-stencil apply (fp64)",
             "value": round(value, 3), "unit": "GDoF/s", "n_gpus": world,

@@ -47,7 +47,9 @@ extern "C" {
 
 /* flags */
 #define HHG_FLAG_RESIDUAL 1 /* write f - A u instead of A u               */
-#define HHG_FLAG_FAST 2     /* FMA / mirror-pair reassociated arithmetic   */
+#define HHG_FLAG_FAST 2     /* FMA / mirror-pair reassociated arithmetic
+                               (scaling and nodal rows; within 1e-12 of
+                               the reference order)                        */
 #define HHG_FLAG_MIRROR 4   /* caller guarantees sh[d] == sh[d+7] bitwise
                                for every element: edge terms shared by two
                                rows are evaluated once (result unchanged)  */

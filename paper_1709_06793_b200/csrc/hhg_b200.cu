@@ -235,6 +235,8 @@ static int dispatch_volume(const VolDesc &D, int variant, int flags, cudaStream_
       return res ? launch_volume<0, SRC, true, false>(D, st)
                  : launch_volume<0, SRC, false, false>(D, st);
     case HHG_VAR_NODAL:
+      if (fast) return res ? launch_volume<1, SRC, true, true>(D, st)
+                           : launch_volume<1, SRC, false, true>(D, st);
       return res ? launch_volume<1, SRC, true, false>(D, st)
                  : launch_volume<1, SRC, false, false>(D, st);
     case HHG_VAR_CONST:

@@ -216,6 +216,42 @@ __device__ __forceinline__ double nodal_row_exact(double v0, double k0,
   return nodal_acc<0>(0.0, v0, q, b, fac);
 }
 
+// FMA form of the nodal row (Operator(fast=True)): the same 40-add element
+// sums, then s_d = fma(b, fac, s) over the terms and acc = fma(s_d,
+// v_q - v0, acc): 140 instead of 211 FP64 operations per row, within 1e-12
+// (max-norm relative) of the reference order
+template <int T, int END, class FAC>
+__device__ __forceinline__ double dir_terms_fma(double s, const double (&b)[55],
+                                                const FAC &fac) {
+  if constexpr (T < END) {
+    constexpr int slot = 31 + Patch::telem[T];
+    return dir_terms_fma<T + 1, END>(fma(b[slot], fac[T], s), b, fac);
+  } else {
+    return s;
+  }
+}
+
+template <int D, class FAC>
+__device__ __forceinline__ double nodal_acc_fma(double acc, double v0, const double2 (&q)[14],
+                                                const double (&b)[55], const FAC &fac) {
+  if constexpr (D < 14) {
+    constexpr int t0 = Patch::tptr[D], t1 = Patch::tptr[D + 1];
+    constexpr int slot = 31 + Patch::telem[t0];
+    const double sd = dir_terms_fma<t0 + 1, t1>(b[slot] * fac[t0], b, fac);
+    return nodal_acc_fma<D + 1>(fma(sd, q[D].x - v0, acc), v0, q, b, fac);
+  } else {
+    return acc;
+  }
+}
+
+template <class FAC>
+__device__ __forceinline__ double nodal_row_fast(double v0, double k0, const double2 (&q)[14],
+                                                 const FAC &fac) {
+  double b[55];
+  nodal_buffer(k0, q, b);
+  return nodal_acc_fma<0>(0.0, v0, q, b, fac);
+}
+
 // dump form (kernels.py:330-376): row[1 + d] = s_d, tot += s_d
 template <int D, class FAC>
 __device__ __forceinline__ void dump_nodal_terms(double &tot, double *row, const double (&b)[55],

@@ -446,7 +446,7 @@ struct RowOp<1, FAST> {  // nodal integration, factors broadcast from smem
   }
   __device__ __forceinline__ double operator()(double v0, double k0, const double2 (&q)[14],
                                                int) const {
-    return nodal_row_exact(v0, k0, q, fac);
+    return FAST ? nodal_row_fast(v0, k0, q, fac) : nodal_row_exact(v0, k0, q, fac);
   }
 };
 

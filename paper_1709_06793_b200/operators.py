@@ -267,7 +267,7 @@ class Operator:
         # reference order)
         if self._mirror and self._vol_variant() == _lib.VAR["scaling"]:
             f |= _lib.FLAG_MIRROR
-        if self.fast and self.variant != "nodal":
+        if self.fast and self._vol_variant() in (_lib.VAR["scaling"], _lib.VAR["nodal"]):
             f |= _lib.FLAG_FAST
         return f
 

@@ -212,13 +212,22 @@ def test_device_tensor_path_and_errors(cuda):
     assert op.flops_add == 3 * 41 * nvol and op.flops_mul == 3 * 28 * nvol
 
 
-def test_fast_mode_within_tolerance(cuda):
+@pytest.mark.parametrize("variant", ["scaling", "nodal"])
+def test_fast_mode_within_tolerance(cuda, variant):
+    """fast=True (FMA edge-flux scaling rows / FMA term sums of the nodal
+    rows) stays within 1e-12 (max-norm relative) of the reference order,
+    for apply and residual."""
     grid = M.RefinedGrid(case_mesh("c3"), 5)
     kf = sample_nodal(k_c3(), grid)
-    u = np.random.default_rng(4).uniform(-1, 1, grid.n_nodes)
-    exact = Operator(grid, "scaling", kf).apply(u)
-    fast = Operator(grid, "scaling", kf, fast=True).apply(u)
+    rng = np.random.default_rng(4)
+    u = rng.uniform(-1, 1, grid.n_nodes)
+    f = rng.uniform(-1, 1, grid.n_nodes)
+    ex, fa = Operator(grid, variant, kf), Operator(grid, variant, kf, fast=True)
+    exact, fast = ex.apply(u), fa.apply(u)
+    assert not np.array_equal(fast, exact)          # the FMA path really ran
     assert np.abs(fast - exact).max() <= 1e-12 * np.abs(exact).max()
+    re, rf = ex.residual(u, f), fa.residual(u, f)
+    assert np.abs(rf - re).max() <= 1e-12 * np.abs(re).max()
 
 
 # -- config 3 at full size (48 macro elements, level 7, 1.7e7 nodes) -----------
