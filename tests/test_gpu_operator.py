@@ -571,17 +571,18 @@ def test_fast_config1_against_oracle(cuda):
 
 
 @pytest.mark.slow
-def test_fast_config3_full_size(cuda):
+@pytest.mark.parametrize("variant", ["scaling", "nodal"])
+def test_fast_config3_full_size(cuda, variant):
     """Config 3 at full size (48 elements, level 7): the FMA path against
-    the bitwise path (itself pinned by test_config3_full_size_checksums),
-    apply and residual."""
+    the bitwise path (itself pinned by test_config3_full_size_checksums and
+    the per-element oracle tests), apply and residual."""
     torch = cuda
     grid = M.RefinedGrid(case_mesh("c3"), 7)
     kf = sample_nodal(k_c3(), grid)
     rng = np.random.default_rng(17)
     u = torch.as_tensor(rng.uniform(-1, 1, grid.n_nodes), device="cuda")
     f = torch.as_tensor(rng.uniform(-1, 1, grid.n_nodes), device="cuda")
-    exact, fast = Operator(grid, "scaling", kf), Operator(grid, "scaling", kf, fast=True)
+    exact, fast = Operator(grid, variant, kf), Operator(grid, variant, kf, fast=True)
     a, b = exact.apply(u), fast.apply(u)
     assert ((a - b).abs().max() / a.abs().max()).item() <= TOL_FAST
     a, b = exact.residual(u, f), fast.residual(u, f)
