@@ -124,8 +124,8 @@ static int launch_mirror(const VolDesc &D, cudaStream_t st) {
 #ifndef HHG_VOLUME_WS
 #define HHG_VOLUME_WS 0          // warp-specialised producer / consumer form
 #endif
-  if (HHG_VOLUME_WS && NW == 4 && MODE == 0) {
-    auto kern = volume_kernel_ws<SRC, RES, kB, kNS>;
+  if (HHG_VOLUME_WS && NW == 4) {
+    auto kern = volume_kernel_ws<SRC, RES, kB, kNS, MODE>;
     if (smem_optin((const void *)kern, (int)smem)) return HHG_ERR_CUDA;
     kern<<<D.nmtiles, 256, smem, st>>>(D);
     return check("volume_kernel_ws");

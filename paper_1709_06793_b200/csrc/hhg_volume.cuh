@@ -1080,7 +1080,7 @@ volume_kernel_mirror(VolDesc D) {
 // stream.  Same tiles, ring, lane layout and arithmetic as the mirror kernel
 // (bitwise equal).  2 CTAs x 8 warps per SM.
 // ---------------------------------------------------------------------------
-template <int SRC, bool RES, int B, int NS>
+template <int SRC, bool RES, int B, int NS, int MODE = 0>
 __global__ void __launch_bounds__(256, 2)
 volume_kernel_ws(VolDesc D) {
   constexpr int NW = 4;                     // consumer warps (8 columns each)
@@ -1196,7 +1196,8 @@ volume_kernel_ws(VolDesc D) {
   }
 
   Win<B> X0, X1, X2;
-  MirrorCarry<B> carry;
+  MirrorCarry<B> carry;   // MODE 0
+  double P[B];            // MODE 1
   auto fetch = [&](int q, Win<B> &w) {
     const int sl = q % NS;
     mbar_wait(full0 + 8 * sl, (q / NS) & 1);
@@ -1221,14 +1222,18 @@ volume_kernel_ws(VolDesc D) {
     fetch(q, hi);
     if (warp_min_ij <= n - q) {
       double vals[B];
-      mirror_step<B>(mi, hi, sh, carry, vals);
+      if constexpr (MODE == 0) mirror_step<B>(mi, hi, sh, carry, vals);
+      else fma_step<B>(mi, hi, sh, P, vals);
       emit(q - 1, vals);
     }
   };
   if (kmax >= 1) {
     fetch(0, X0);
     fetch(1, X1);
-    if (warp_min_ij <= n - 2) mirror_seed<B>(X0, X1, sh, carry);
+    if (warp_min_ij <= n - 2) {
+      if constexpr (MODE == 0) mirror_seed<B>(X0, X1, sh, carry);
+      else fma_seed<B>(X0, X1, sh, P);
+    }
     step(2, X1, X2);
     for (int q = 3; q <= kmax + 1; q += 3) {
       step(q, X2, X0);
