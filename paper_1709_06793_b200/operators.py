@@ -407,7 +407,11 @@ class Operator:
             grid, dg = self.grid, D["grid"]
             ne = grid.macro.n_elements
             ng = max(1, min(groups, ne))
-            bounds = np.linspace(0, ne, ng + 1).astype(int)
+            # the first group is a single element: the D2H leg can start as
+            # soon as the surface block and one volume block have landed
+            bounds = np.unique(np.concatenate(
+                [[0], np.linspace(min(1, ne), ne, ng).astype(int)])) if ne > 1 else \
+                np.array([0, ne])
             tiles, mtiles = dg.gt.tiles, dg.gt.mtiles
             descs, keep = [], []
             for g in range(ng):
