@@ -485,11 +485,14 @@ struct Hyperplanes {
   // the boundary (ghost) points: code and position in that order
   int *bcode = nullptr, *bpos = nullptr;
   int nb = 0;
+  // interior points in volume-block (k, j, i) order (the scatter back to u)
+  int *icode = nullptr;
 };
 
 static int hyperplanes(int n, const int **ptr, const int **code, const int **xstart = nullptr,
                        const int **xcode = nullptr, const int **bcode = nullptr,
-                       const int **bpos = nullptr, int *nb = nullptr) {
+                       const int **bpos = nullptr, int *nb = nullptr,
+                       const int **icode = nullptr) {
   static std::map<std::pair<int, int>, Hyperplanes> cache;
   std::lock_guard<std::mutex> lock(g_cache_mu);
   const auto key = std::make_pair(current_device(), n);
@@ -506,6 +509,10 @@ static int hyperplanes(int n, const int **ptr, const int **code, const int **xst
         }
     }
     if (hmax >= hmin) p[hmax - hmin + 1] = (int)c.size();
+    std::vector<int> ic;
+    for (int k = 1; k <= n - 3; ++k)
+      for (int j = 1; j <= n - 2 - k; ++j)
+        for (int i = 1; i <= n - 1 - j - k; ++i) ic.push_back(i | (j << 10) | (k << 20));
     std::vector<int> xs((3 * n + 1) * (n + 1), 0), xc, bc, bp;
     for (int h = 0; h <= 3 * n; ++h)
       for (int k = 0; k <= n; ++k) {
@@ -532,6 +539,7 @@ static int hyperplanes(int n, const int **ptr, const int **code, const int **xst
     if (!rc) rc = upload(xc, &hp.xcode);
     if (!rc) rc = upload(bc, &hp.bcode);
     if (!rc) rc = upload(bp, &hp.bpos);
+    if (!rc) rc = upload(ic, &hp.icode);
     if (rc) return rc;
     hp.nb = (int)bc.size();
     it = cache.emplace(key, hp).first;
@@ -543,6 +551,7 @@ static int hyperplanes(int n, const int **ptr, const int **code, const int **xst
   if (bcode) *bcode = it->second.bcode;
   if (bpos) *bpos = it->second.bpos;
   if (nb) *nb = it->second.nb;
+  if (icode) *icode = it->second.icode;
   return HHG_OK;
 }
 
@@ -1133,8 +1142,9 @@ int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef, d
   if (!us || !fs || !ks) return HHG_ERR_ARG;
   GSDesc G = gs_grid_desc(g, variant, coef, omega, u, f);
   const int *xstart = nullptr, *xcode = nullptr, *bcode = nullptr, *bpos = nullptr;
+  const int *icode = nullptr;
   int nb = 0;
-  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code, &xstart, &xcode, &bcode, &bpos, &nb);
+  int rc = hyperplanes(g->n, &G.hp_ptr, &G.hp_code, &xstart, &xcode, &bcode, &bpos, &nb, &icode);
   if (rc) return rc;
   const dim3 mx((int)((G.L + 255) / 256), g->ntets);
   if (flags & HHG_SKEW_U_CURRENT) {     // interior of us current: ghost values only
@@ -1201,7 +1211,11 @@ int hhg_smooth_volume_skew(const hhg_grid *g, int variant, const double *coef, d
     fprintf(stderr, "hhg_b200: gs_volume_skew_kernel: %s\n", cudaGetErrorString(e));
     return HHG_ERR_CUDA;
   }
-  skew_move_kernel<1><<<mx, 256, 0, S(stream)>>>(G, xcode, us, u);
+  if (HHG_SKEW_SCATTER_LAT)       // volume-block order: full-sector writes into u
+    skew_scatter_kernel<<<dim3((int)((g->nvol + 255) / 256), g->ntets), 256, 0, S(stream)>>>(
+        G, icode, xstart, us, u);
+  else
+    skew_move_kernel<1><<<mx, 256, 0, S(stream)>>>(G, xcode, us, u);
   return check("skew_move_kernel");
 }
 

@@ -383,6 +383,27 @@ __global__ void skew_move_kernel(GSDesc D, const int *__restrict__ xcode,
   }
 }
 
+// The scatter back to u walked in u's own (volume-block) order: the
+// writes fill whole sectors and the 8-byte reads of the skewed copy are
+// the scattered side (L2 hits: an element's copy is ~23 MB), where
+// skew_move_kernel<1> wrote u one scattered 8-byte word per thread
+// (partial-sector writes: L2 at 73% of its peak, DRAM at 31%).
+#ifndef HHG_SKEW_SCATTER_LAT
+#define HHG_SKEW_SCATTER_LAT 1
+#endif
+__global__ void skew_scatter_kernel(GSDesc D, const int *__restrict__ icode,
+                                    const int *__restrict__ xstart, const double *__restrict__ us,
+                                    double *__restrict__ u) {
+  const int t = blockIdx.y;
+  const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (c >= D.nvol) return;
+  const int n = D.n;
+  const int code = __ldg(icode + c);
+  const int i = code & 1023, j = (code >> 10) & 1023, k = (code >> 20) & 1023;
+  const int pos = __ldg(xstart + (i + 2 * j + 3 * k) * (n + 1) + k) + j;
+  u[D.vol_start[t] + c] = __ldg(us + (long long)t * D.L + pos);
+}
+
 // refresh the boundary (ghost) points of us only: the interior is current
 // (the previous sweep of the same smoothing left it equal to u)
 __global__ void skew_boundary_kernel(GSDesc D, const int *__restrict__ bcode,
