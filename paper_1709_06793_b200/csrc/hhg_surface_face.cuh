@@ -56,22 +56,36 @@ surface_face_kernel(SurfGSDesc G, const hhg_surface s, double *out, SurfPush pus
     const int l = F.dl[e][d];
     offs[e][d] = l < 0 ? NONE : (l == 0 ? 0 : 1 + e) * AREA + F.db[e][d] * FACE_W + F.da[e][d];
   }
-  // stage: static k and global ids of the layers, u gathered through them
+  // stage: static k and global ids of the layers, u gathered through them.
+  // All of a thread's id and k loads are issued first, then all its u
+  // gathers: two dependent round trips per thread instead of two per point.
   const long long layer0 = (long long)tl.x * 3 * sq * sq;
-  for (int x = threadIdx.x; x < (1 + ne) * AREA; x += blockDim.x) {
+  constexpr int NT = FACE_TA * FACE_TB, NIT = (3 * AREA + NT - 1) / NT;
+  const int nx = (1 + ne) * AREA;
+  const unsigned *gbase = reinterpret_cast<const unsigned *>(s.face_g) + layer0;
+  const double *kbase = s.face_k + layer0;
+  unsigned sg[NIT];
+  double kv[NIT];
+  int li[NIT];                                  // layer-local square index, -1: zero slot
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int x = threadIdx.x + it * NT;
     const int l = x / AREA, rem = x - l * AREA;
     const int rb = rem / FACE_W, ra = rem - rb * FACE_W;
-    // square index of (a, b) = (a0 - 1 + ra, b0 - 1 + rb): (b + 1) sq + a + 1
-    if (a0 + ra >= sq || b0 + rb >= sq) {      // past the face's (n+3)^2 square
-      Ls[x] = make_double2(0.0, 0.0);
-      continue;
+    // square index of (a, b) = (a0 - 1 + ra, b0 - 1 + rb): (b + 1) sq + a + 1;
+    // slots past the face's (n+3)^2 square stay zero
+    li[it] = (x < nx && a0 + ra < sq && b0 + rb < sq) ? l * sq * sq + (b0 + rb) * sq + (a0 + ra) : -1;
+    if (li[it] >= 0) {
+      HHG_BOUND(li[it], 0, 3LL * sq * sq, "face staging: layer index");
+      sg[it] = __ldg(gbase + li[it]);
+      kv[it] = __ldg(kbase + li[it]);
     }
-    const long long idx = layer0 + (long long)l * sq * sq + (long long)(b0 + rb) * sq + (a0 + ra);
-    HHG_BOUND(idx - layer0, 0, 3LL * sq * sq, "face staging: layer index");
-    const double kv = __ldg(s.face_k + idx);
-    HHG_BOUND(__ldg(s.face_g + idx), 0, 0xffffffffLL, "face staging: global id");
-    const double v = __ldg(D.u + (unsigned)__ldg(s.face_g + idx));
-    Ls[x] = make_double2(v, kv);
+  }
+#pragma unroll
+  for (int it = 0; it < NIT; ++it) {
+    const int x = threadIdx.x + it * NT;
+    if (li[it] >= 0) Ls[x] = make_double2(__ldg(D.u + sg[it]), kv[it]);
+    else if (x < nx) Ls[x] = make_double2(0.0, 0.0);
   }
   __syncthreads();
   const int ta = threadIdx.x % FACE_TA, tb = threadIdx.x / FACE_TA;
