@@ -98,22 +98,28 @@ surface_face_kernel(SurfGSDesc G, const hhg_surface s, double *out, SurfPush pus
   for (int e = 0; e < ne; ++e) {
     const int t = F.tet[e], cls = F.cls[e];
     const unsigned mask = c_cls_dirmask[cls];
-    double2 q[14];
-#pragma unroll
-    for (int d = 0; d < 14; ++d) {
-      const int o = offs[e][d];
-      if (o != NONE) HHG_BOUND(ctr + o, 0, 3 * AREA, "face row: staged neighbour");
-      q[d] = o == NONE ? make_double2(v0, 0.0) : Ls[ctr + o];
-    }
     double part;
     if (!MIXED || !F.nodal) {
+      // only the directions of the one-sided stencil are read (all of them
+      // stay inside the element, so their offsets are never NONE)
       const double *sh = D.psh + ((long long)t * 14 + cls) * 14;
       part = 0.0;
 #pragma unroll
       for (int d = 0; d < 14; ++d)
-        if (mask >> d & 1)
-          part = dadd(part, dmul(dmul(dadd(c0.y, q[d].y), __ldg(sh + d)), dsub(q[d].x, v0)));
+        if (mask >> d & 1) {
+          const int o = offs[e][d];
+          HHG_BOUND(ctr + o, 0, 3 * AREA, "face row: staged neighbour");
+          const double2 q = Ls[ctr + o];
+          part = dadd(part, dmul(dmul(dadd(c0.y, q.y), __ldg(sh + d)), dsub(q.x, v0)));
+        }
     } else {
+      double2 q[14];
+#pragma unroll
+      for (int d = 0; d < 14; ++d) {
+        const int o = offs[e][d];
+        if (o != NONE) HHG_BOUND(ctr + o, 0, 3 * AREA, "face row: staged neighbour");
+        q[d] = o == NONE ? make_double2(v0, 0.0) : Ls[ctr + o];
+      }
       const double *fac = D.pfac + ((long long)t * 14 + cls) * 72;
       part = nodal_row_exact(v0, c0.y, q, fac);
     }
